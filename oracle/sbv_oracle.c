@@ -1,0 +1,465 @@
+/*
+ * sbv_oracle.c — plain, slow, obviously-correct FP64 CPU oracle for the
+ * Scaled Block Vecchia (SBV) log-likelihood hot path (arXiv 2504.12004).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * The product path (paper_2504_12004_b200, libsbv.so) never links, imports
+ * or executes anything in oracle/, and this file includes nothing from it.
+ *
+ * Citation convention: "P:a-b" = /root/reference/PAPER.md lines a-b,
+ * "S:a-b" = SPEC.md lines a-b.  Readings of ambiguous passages are the
+ * numbered Q-readings listed in DESIGN.md ("Readings of the paper").
+ *
+ * Each step follows the paper's algorithm in the paper's order, written out
+ * with no blocking, fusion or reordering:
+ *   O1 orc_scale        Alg.2 line 7, Eq.5
+ *   O2 orc_anchors      Alg.3 line 4 + Alg.1 line 9 random reorder
+ *   O3 orc_rac          Alg.3 line 5
+ *   O4 orc_layout       blocks as contiguous member lists
+ *   O5 orc_centroids    Alg.4 line 6
+ *   O6 orc_knn_block    Eq.2 with Alg.4 lines 15-27,
+ *                       exact m-NN over all strictly-earlier blocks (Q5, Q6, Q13)
+ *   O7 orc_kernel       Eq.5 + Eq.6, half-integer nu closed forms (Q4)
+ *   O8 orc_block_term   Alg.5 literally, Sigma_new = Sigma_lk - Sigma_cor (Q1),
+ *                       with the -(bs/2) log 2pi constant of Eq.1 (Q2)
+ *   O9 orc_loglik       Alg.1 Step 4-5: sum of block terms in zeta order
+ *                       (Neumaier-compensated, Q15)
+ *
+ * Pins (tests/test_oracle_*.py) tie every function to something other than
+ * itself: splitmix64 published vectors, scipy.special.kv Matern, dense Eq.1
+ * under full conditioning, explicit-inverse conditionals, brute-force kNN and
+ * RAC (exact lattice data), closed forms for n=1/2, the variance scaling law,
+ * and KL >= 0 monotone in m (Eq.4).  The absolute loglik at the benchmark
+ * configs has no printed value in the paper: beyond those pins it is
+ * "parity unpinned".
+ *
+ * Build: gcc -O2 -ffp-contract=off -fopenmp -shared -fPIC  (no FMA contraction
+ * except the explicit fma() calls of the distance chain, Q14).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORC_OK 0
+#define ORC_ERR_ARG 1
+#define ORC_ERR_NOT_PD 4
+#define ORC_ERR_UNSUPPORTED 5
+
+/* ------------------------------------------------------------------ O1 */
+/* Alg.2 line 7: X_{p,j} := X^org_{p,j} / beta_j.  IEEE division,
+ * never a multiplication by a reciprocal (Q14). */
+void orc_scale(const double *X, int64_t n, int32_t d, const double *scale,
+               double *S) {
+  for (int64_t i = 0; i < n; i++)
+    for (int32_t j = 0; j < d; j++) S[i * d + j] = X[i * d + j] / scale[j];
+}
+
+/* ------------------------------------------------------------------ O2 */
+/* splitmix64: the i-th output (i = 0, 1, ...) of the generator seeded with
+ * `seed` (state advanced by the golden gamma before each output).  Q9. */
+uint64_t orc_splitmix64(uint64_t seed, uint64_t i) {
+  uint64_t z = seed + (i + 1) * 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+/* k = round(n / bs) with halves rounded up, at least 1 (Q8). */
+int64_t orc_num_blocks(int64_t n, int32_t bs) {
+  int64_t k = (2 * n + bs) / (2 * (int64_t)bs); /* floor(n/bs + 1/2) */
+  return k < 1 ? 1 : k;
+}
+
+typedef struct {
+  uint64_t key;
+  int64_t i;
+} orc_keyidx;
+
+static int cmp_keyidx(const void *a, const void *b) {
+  const orc_keyidx *x = (const orc_keyidx *)a, *y = (const orc_keyidx *)b;
+  if (x->key != y->key) return x->key < y->key ? -1 : 1;
+  return x->i < y->i ? -1 : (x->i > y->i);
+}
+
+/* Alg.3 line 4 "Randomly choose k_p local centers" and Alg.1 line 9
+ * "Randomly reorder these blocks": the anchors are the k points with the
+ * smallest (key(i), i); anchor rank r seeds block r and block r has zeta
+ * position r (Q8, Q9). */
+void orc_anchors(int64_t n, int64_t k, uint64_t seed, int32_t *anchors) {
+  orc_keyidx *a = (orc_keyidx *)malloc(sizeof(orc_keyidx) * n);
+  for (int64_t i = 0; i < n; i++) {
+    a[i].key = orc_splitmix64(seed, (uint64_t)i);
+    a[i].i = i;
+  }
+  qsort(a, n, sizeof(orc_keyidx), cmp_keyidx);
+  for (int64_t r = 0; r < k; r++) anchors[r] = (int32_t)a[r].i;
+  free(a);
+}
+
+/* ------------------------------------------------------------------ O3 */
+/* Squared Euclidean distance in scaled space as the explicit fma chain in
+ * dimension order (Q14): acc = 0; acc = fma(t, t, acc). */
+double orc_dist2(const double *a, const double *b, int32_t d) {
+  double acc = 0.0;
+  for (int32_t j = 0; j < d; j++) {
+    double t = a[j] - b[j];
+    acc = fma(t, t, acc);
+  }
+  return acc;
+}
+
+/* Alg.3 line 5: assign x_i to argmin_j ||x_i - c_j||^2, ties to
+ * the lowest anchor rank; an anchor belongs to its own block. */
+void orc_rac(const double *S, int64_t n, int32_t d, const int32_t *anchors,
+             int64_t k, int32_t *block_of) {
+  for (int64_t i = 0; i < n; i++) block_of[i] = -1;
+  for (int64_t r = 0; r < k; r++) block_of[anchors[r]] = (int32_t)r;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; i++) {
+    if (block_of[i] >= 0) continue;
+    double best = INFINITY;
+    int64_t arg = -1;
+    for (int64_t r = 0; r < k; r++) {
+      double d2 = orc_dist2(S + i * d, S + (int64_t)anchors[r] * d, d);
+      if (d2 < best) { /* strict: the first (lowest r) minimum wins */
+        best = d2;
+        arg = r;
+      }
+    }
+    block_of[i] = (int32_t)arg;
+  }
+}
+
+/* ------------------------------------------------------------------ O4 */
+/* Block-major layout: block t occupies perm[off[t] .. off[t+1]), members in
+ * ascending original index (Q13). */
+void orc_layout(const int32_t *block_of, int64_t n, int64_t k, int32_t *perm,
+                int64_t *off) {
+  int64_t *cnt = (int64_t *)calloc(k + 1, sizeof(int64_t));
+  for (int64_t i = 0; i < n; i++) cnt[block_of[i]]++;
+  off[0] = 0;
+  for (int64_t t = 0; t < k; t++) off[t + 1] = off[t] + cnt[t];
+  for (int64_t t = 0; t < k; t++) cnt[t] = off[t];
+  for (int64_t i = 0; i < n; i++) perm[cnt[block_of[i]]++] = (int32_t)i;
+  free(cnt);
+}
+
+/* ------------------------------------------------------------------ O5 */
+/* Alg.4 line 6: c_t = (1/|B_t|) sum_{x in B_t} x, summed left to
+ * right over members in ascending index, one division. */
+void orc_centroids(const double *S, int32_t d, const int32_t *perm,
+                   const int64_t *off, int64_t k, double *C) {
+  for (int64_t t = 0; t < k; t++) {
+    for (int32_t j = 0; j < d; j++) {
+      double s = 0.0;
+      for (int64_t p = off[t]; p < off[t + 1]; p++)
+        s = s + S[(int64_t)perm[p] * d + j];
+      C[t * d + j] = s / (double)(off[t + 1] - off[t]);
+    }
+  }
+}
+
+/* ------------------------------------------------------------------ O6 */
+typedef struct {
+  double d2;
+  int64_t idx;
+} orc_cand;
+
+static int cmp_cand(const void *a, const void *b) {
+  const orc_cand *x = (const orc_cand *)a, *y = (const orc_cand *)b;
+  if (x->d2 != y->d2) return x->d2 < y->d2 ? -1 : 1;
+  return x->idx < y->idx ? -1 : (x->idx > y->idx);
+}
+
+/* Eq.2 NN(B_t) with Alg.4's ordering constraint read as STRICTLY earlier
+ * blocks (Q5) and the member-mean centroid as the query (Q6): all points of
+ * blocks 0..t-1 are candidates, fully sorted by (dist2(c_t, s), index) and
+ * the first min(m, off[t]) kept, in that order.  nbr_t receives ORIGINAL
+ * point indices, -1 padded to m.  Returns the count. */
+int32_t orc_knn_block(const double *S, int32_t d, const int32_t *perm,
+                      const int64_t *off, const double *C, int64_t t,
+                      int32_t m, int32_t *nbr_t) {
+  int64_t A = off[t];
+  int32_t cnt = (int32_t)(A < m ? A : m);
+  for (int32_t j = 0; j < m; j++) nbr_t[j] = -1;
+  if (A == 0) return 0;
+  orc_cand *c = (orc_cand *)malloc(sizeof(orc_cand) * A);
+  for (int64_t p = 0; p < A; p++) {
+    c[p].idx = perm[p];
+    c[p].d2 = orc_dist2(C + t * d, S + (int64_t)perm[p] * d, d);
+  }
+  qsort(c, A, sizeof(orc_cand), cmp_cand);
+  for (int32_t j = 0; j < cnt; j++) nbr_t[j] = (int32_t)c[j].idx;
+  free(c);
+  return cnt;
+}
+
+void orc_knn(const double *S, int32_t d, const int32_t *perm,
+             const int64_t *off, const double *C, int64_t k, int32_t m,
+             int32_t *nbr, int32_t *cnt, int32_t nthreads) {
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic)
+  for (int64_t t = 0; t < k; t++)
+    cnt[t] = orc_knn_block(S, d, perm, off, C, t, m, nbr + t * (int64_t)m);
+}
+
+/* ------------------------------------------------------------------ O7 */
+/* Eq.6 in the paper's parameterisation (no sqrt(2 nu), Q4):
+ * f(r) = sigma2 * 2^{1-nu}/Gamma(nu) * r^nu K_nu(r), written in the
+ * half-integer closed forms; r = 0 limit is sigma2. */
+double orc_matern(double r, double sigma2, double nu) {
+  double e = exp(-r);
+  if (nu == 0.5) return sigma2 * e;
+  if (nu == 1.5) return sigma2 * (1.0 + r) * e;
+  if (nu == 2.5) return sigma2 * (1.0 + r + r * r / 3.0) * e;
+  if (nu == 3.5)
+    return sigma2 * (1.0 + r + 2.0 * r * r / 5.0 + r * r * r / 15.0) * e;
+  return NAN;
+}
+
+/* Eq.5: r = ( sum_i (x_ki - x_k'i)^2 / beta_i^2 )^{1/2} on the
+ * ORIGINAL inputs with theta's beta (Q11).  theta = {sigma2, beta_1..beta_d,
+ * nu, tau2}.  The nugget tau2 is added only when the two
+ * arguments are the same point of a same-set matrix (Q3). */
+double orc_scaled_distance(const double *xa, const double *xb, int32_t d,
+                           const double *beta) {
+  double acc = 0.0;
+  for (int32_t i = 0; i < d; i++) {
+    double t = xa[i] - xb[i];
+    acc = acc + (t * t) / (beta[i] * beta[i]);
+  }
+  return sqrt(acc);
+}
+
+double orc_kernel(const double *xa, const double *xb, int32_t d,
+                  const double *theta, int32_t same_point) {
+  double r = orc_scaled_distance(xa, xb, d, theta + 1);
+  double v = orc_matern(r, theta[0], theta[d + 1]);
+  if (same_point) v = v + theta[d + 2];
+  return v;
+}
+
+/* ------------------------------------------------------------------ O8 */
+/* Unblocked Cholesky-Banachiewicz of the n x n row-major SPD matrix A in
+ * place (lower triangle).  Returns 0 or (pivot index + 1) on a non-positive
+ * pivot. */
+static int64_t chol_lower(double *A, int64_t n) {
+  for (int64_t i = 0; i < n; i++) {
+    for (int64_t j = 0; j <= i; j++) {
+      double s = A[i * n + j];
+      for (int64_t q = 0; q < j; q++) s = s - A[i * n + q] * A[j * n + q];
+      if (i == j) {
+        if (!(s > 0.0)) return i + 1;
+        A[i * n + i] = sqrt(s);
+      } else {
+        A[i * n + j] = s / A[j * n + j];
+      }
+    }
+  }
+  return 0;
+}
+
+/* Forward substitution L z = b, L lower n x n row-major; b overwritten. */
+static void forward_subst(const double *L, int64_t n, double *b) {
+  for (int64_t i = 0; i < n; i++) {
+    double s = b[i];
+    for (int64_t q = 0; q < i; q++) s = s - L[i * n + q] * b[q];
+    b[i] = s / L[i * n + i];
+  }
+}
+
+/* Alg.5 for ONE block, literally:
+ *   Sigma_lk    = K(B, B)            bs x bs   (nugget on its diagonal)
+ *   Sigma_con   = K(J, J)            m x m     (nugget on its diagonal)
+ *   Sigma_cross = K(J, B)            m x bs    (no nugget)
+ *   L           = POTRF(Sigma_con)
+ *   Sigma'cross = TRSM(L, Sigma_cross)        = L^-1 Sigma_cross
+ *   y'_J        = TRSV(L, y_J)                = L^-1 y_J
+ *   Sigma_cor   = Sigma'cross^T Sigma'cross   (GEMM)
+ *   mu_cor      = Sigma'cross^T y'_J          (GEMV)
+ *   Sigma_new   = Sigma_lk - Sigma_cor        (Q1: printed "Sigma_con")
+ *   L'          = POTRF(Sigma_new)
+ *   v           = TRSV(L', y_B - mu_new)
+ *   u = v^T v,  dlog = 2 sum log L'_jj
+ *   term = -(1/2)(u + dlog) - (bs/2) log(2 pi)   (Q2)
+ * J = original indices of the conditioning set in kNN order, B = original
+ * indices of the block members ascending.  With m_t = 0 this is the
+ * marginal N(y_B; 0, Sigma_lk).  Returns ORC_OK or ORC_ERR_NOT_PD with
+ * *stage = 1 (Sigma_con) or 2 (Sigma_new). */
+int orc_block_term(const double *X, const double *y, int32_t d,
+                   const int32_t *J, int32_t mt, const int32_t *B, int32_t bst,
+                   const double *theta, double *term, double *quad,
+                   double *logdet, int32_t *stage) {
+  int64_t m = mt, b = bst;
+  double *Slk = (double *)malloc(sizeof(double) * b * b);
+  double *Scon = (double *)malloc(sizeof(double) * (m > 0 ? m * m : 1));
+  double *Scross = (double *)malloc(sizeof(double) * (m > 0 ? m * b : 1));
+  double *yJ = (double *)malloc(sizeof(double) * (m > 0 ? m : 1));
+  double *Scor = (double *)malloc(sizeof(double) * b * b);
+  double *mu = (double *)malloc(sizeof(double) * b);
+  double *v = (double *)malloc(sizeof(double) * b);
+  int rc = ORC_OK;
+  *stage = 0;
+
+  for (int64_t i = 0; i < b; i++)
+    for (int64_t j = 0; j < b; j++)
+      Slk[i * b + j] = orc_kernel(X + (int64_t)B[i] * d, X + (int64_t)B[j] * d,
+                                  d, theta, i == j);
+  for (int64_t i = 0; i < m; i++)
+    for (int64_t j = 0; j < m; j++)
+      Scon[i * m + j] = orc_kernel(X + (int64_t)J[i] * d,
+                                   X + (int64_t)J[j] * d, d, theta, i == j);
+  for (int64_t i = 0; i < m; i++)
+    for (int64_t j = 0; j < b; j++)
+      Scross[i * b + j] = orc_kernel(X + (int64_t)J[i] * d,
+                                     X + (int64_t)B[j] * d, d, theta, 0);
+  for (int64_t i = 0; i < m; i++) yJ[i] = y[J[i]];
+
+  for (int64_t i = 0; i < b * b; i++) Scor[i] = 0.0;
+  for (int64_t i = 0; i < b; i++) mu[i] = 0.0;
+  if (m > 0) {
+    if (chol_lower(Scon, m) != 0) { /* L = POTRF(Sigma_con) */
+      rc = ORC_ERR_NOT_PD;
+      *stage = 1;
+      goto done;
+    }
+    /* Sigma'cross = L^-1 Sigma_cross, one column at a time */
+    double *col = (double *)malloc(sizeof(double) * m);
+    for (int64_t j = 0; j < b; j++) {
+      for (int64_t i = 0; i < m; i++) col[i] = Scross[i * b + j];
+      forward_subst(Scon, m, col);
+      for (int64_t i = 0; i < m; i++) Scross[i * b + j] = col[i];
+    }
+    free(col);
+    forward_subst(Scon, m, yJ); /* y'_J = L^-1 y_J */
+    for (int64_t i = 0; i < b; i++) /* Sigma_cor = Sigma'cross^T Sigma'cross */
+      for (int64_t j = 0; j < b; j++) {
+        double s = 0.0;
+        for (int64_t q = 0; q < m; q++)
+          s = s + Scross[q * b + i] * Scross[q * b + j];
+        Scor[i * b + j] = s;
+      }
+    for (int64_t i = 0; i < b; i++) { /* mu_cor = Sigma'cross^T y'_J */
+      double s = 0.0;
+      for (int64_t q = 0; q < m; q++) s = s + Scross[q * b + i] * yJ[q];
+      mu[i] = s;
+    }
+  }
+  for (int64_t i = 0; i < b * b; i++) Slk[i] = Slk[i] - Scor[i]; /* Sigma_new */
+  if (chol_lower(Slk, b) != 0) {                                 /* L' */
+    rc = ORC_ERR_NOT_PD;
+    *stage = 2;
+    goto done;
+  }
+  for (int64_t i = 0; i < b; i++) v[i] = y[B[i]] - mu[i];
+  forward_subst(Slk, b, v); /* v = L'^-1 (y_B - mu_new) */
+  {
+    double u = 0.0, dl = 0.0;
+    for (int64_t i = 0; i < b; i++) u = u + v[i] * v[i];
+    for (int64_t i = 0; i < b; i++) dl = dl + log(Slk[i * b + i]);
+    dl = 2.0 * dl;
+    *quad = u;
+    *logdet = dl;
+    *term = -0.5 * (u + dl) - 0.5 * (double)b * log(2.0 * M_PI);
+  }
+done:
+  free(Slk);
+  free(Scon);
+  free(Scross);
+  free(yJ);
+  free(Scor);
+  free(mu);
+  free(v);
+  return rc;
+}
+
+/* ------------------------------------------------------------------ O9 */
+/* Alg.1 Steps 4-5: ell = sum_t ell_t, summed in zeta order with
+ * Neumaier compensation (Q15).  Block t's members are perm[off[t]..off[t+1]),
+ * its conditioning set nbr[t*m .. t*m+cnt[t]) (original indices).  terms may
+ * be NULL.  out[0..2] = {ell, sum quad, sum logdet}.  On a Cholesky failure
+ * returns ORC_ERR_NOT_PD with the lowest failing block and its stage. */
+int orc_loglik(const double *X, const double *y, int64_t n, int32_t d,
+               const int32_t *perm, const int64_t *off, int64_t k,
+               const int32_t *nbr, const int32_t *cnt, int32_t m,
+               const double *theta, int32_t nthreads, double *terms,
+               double *quads, double *logdets, double *out,
+               int64_t *fail_block, int32_t *fail_stage) {
+  (void)n;
+  double *tt = (double *)malloc(sizeof(double) * k);
+  double *qq = (double *)malloc(sizeof(double) * k);
+  double *ll = (double *)malloc(sizeof(double) * k);
+  int32_t *st = (int32_t *)calloc(k, sizeof(int32_t));
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic)
+  for (int64_t t = 0; t < k; t++) {
+    int32_t stage = 0;
+    double term = NAN, quad = NAN, logdet = NAN;
+    orc_block_term(X, y, d, nbr + t * (int64_t)m, cnt[t], perm + off[t],
+                   (int32_t)(off[t + 1] - off[t]), theta, &term, &quad,
+                   &logdet, &stage);
+    tt[t] = term;
+    qq[t] = quad;
+    ll[t] = logdet;
+    st[t] = stage;
+  }
+  int rc = ORC_OK;
+  *fail_block = -1;
+  *fail_stage = 0;
+  double s = 0.0, c = 0.0, sq = 0.0, sl = 0.0;
+  for (int64_t t = 0; t < k; t++) {
+    if (st[t] != 0) {
+      rc = ORC_ERR_NOT_PD;
+      *fail_block = t;
+      *fail_stage = st[t];
+      break;
+    }
+    double x = tt[t], u = s + x; /* Neumaier */
+    if (fabs(s) >= fabs(x))
+      c = c + ((s - u) + x);
+    else
+      c = c + ((x - u) + s);
+    s = u;
+    sq = sq + qq[t];
+    sl = sl + ll[t];
+  }
+  out[0] = rc == ORC_OK ? s + c : NAN;
+  out[1] = sq;
+  out[2] = sl;
+  if (terms) memcpy(terms, tt, sizeof(double) * k);
+  if (quads) memcpy(quads, qq, sizeof(double) * k);
+  if (logdets) memcpy(logdets, ll, sizeof(double) * k);
+  free(tt);
+  free(qq);
+  free(ll);
+  free(st);
+  return rc;
+}
+
+/* Single-block variant used by sampled parity checks at full size. */
+int orc_block_term_at(const double *X, const double *y, int32_t d,
+                      const int32_t *perm, const int64_t *off,
+                      const int32_t *nbr, const int32_t *cnt, int32_t m,
+                      int64_t t, const double *theta, double *term,
+                      double *quad, double *logdet, int32_t *stage) {
+  return orc_block_term(X, y, d, nbr + t * (int64_t)m, cnt[t], perm + off[t],
+                        (int32_t)(off[t + 1] - off[t]), theta, term, quad,
+                        logdet, stage);
+}
+
+int orc_max_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
