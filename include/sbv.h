@@ -1,0 +1,176 @@
+/*
+ * sbv.h — C ABI of libsbv, the B200 (sm_100a) implementation of the Scaled
+ * Block Vecchia log-likelihood hot path (arXiv 2504.12004).
+ *
+ * The calls follow the paper's statement of the problem, Alg.1 (PAPER.md
+ * P:253-288): "Input: data {x_i, y_i}, dimension d, total block count K,
+ * nearest neighbors m_est, workers P, covariance function K_theta, scaling
+ * parameters beta.  Output: the log-likelihood".  sbv_prepare performs
+ * Alg.1 Steps 1-3 (scaling Alg.2, Random Anchor Clustering Alg.3
+ * P:344-360, random block order P:269, m-NN search Alg.4);
+ * sbv_loglik performs Step 4 (batched block log-likelihoods Alg.5
+ * P:462-499) and Step 5 (reduction across workers).
+ *
+ * Conventions for every call:
+ *  - Every entry point returns an sbv_status; nothing throws across the ABI.
+ *    On failure the handle (if any) keeps a message for sbv_last_error.
+ *  - Pointers to bulk arrays (X, y, outputs of sbv_get_*) may be HOST or
+ *    DEVICE pointers: the library inspects them with cudaPointerGetAttributes
+ *    and copies host data to/from the device itself.  They are read/written
+ *    only during the call; the caller keeps ownership.
+ *  - Small parameter arrays (scale, theta) are always host arrays.
+ *  - All FP data is IEEE binary64, row-major, contiguous.
+ *  - A handle is bound to the CUDA device current at sbv_create / sbv_prepare
+ *    and to the stream given in sbv_opts (NULL = the legacy default stream).
+ *    It is not thread-safe: one handle per host thread / stream.
+ *  - There is no CPU fallback: without a usable CUDA device every call that
+ *    needs one returns SBV_ERR_CUDA.
+ */
+#ifndef SBV_H_
+#define SBV_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SBV_ABI_VERSION 1
+#define SBV_MAX_D 64    /* 1 <= d <= 64 */
+
+typedef struct sbv_ctx *sbv_handle; /* opaque; owned by the library */
+
+typedef enum {
+  SBV_OK = 0,
+  SBV_ERR_ARG = 1,         /* invalid argument (sizes, NaN/Inf, beta<=0, ...) */
+  SBV_ERR_CUDA = 2,        /* CUDA runtime error or no device */
+  SBV_ERR_OOM = 3,         /* device allocation failed */
+  SBV_ERR_NOT_PD = 4,      /* a Cholesky pivot was <= 0: see sbv_last_error */
+  SBV_ERR_UNSUPPORTED = 5, /* nu not in {0.5,1.5,2.5,3.5}, or shape beyond kernel limits */
+  SBV_ERR_COMM = 6,        /* NCCL failure */
+  SBV_ERR_STATE = 7        /* call out of order (e.g. loglik before prepare) */
+} sbv_status;
+
+typedef struct {
+  uint64_t seed;   /* RAC anchor / block-order seed (Q9); default 3 */
+  void *stream;    /* cudaStream_t for every launch of this handle; NULL = default */
+  int32_t profile; /* 1 = record per-stage CUDA events (sbv_stage_times) */
+} sbv_opts;
+
+/* ---------------------------------------------------------------- lifecycle */
+
+/* Create an empty handle on the current CUDA device.  opts may be NULL
+ * (seed 3, default stream, no profiling). */
+int sbv_create(const sbv_opts *opts, sbv_handle *out);
+
+/* Free every device buffer and the NCCL communicator.  NULL is a no-op. */
+void sbv_destroy(sbv_handle h);
+
+/* Multi-GPU (one process per GPU, Alg.1 "workers P"): attach an NCCL
+ * communicator made from a 128-byte ncclUniqueId that rank 0 obtained with
+ * sbv_comm_unique_id and broadcast.  Must precede sbv_prepare_h.  Blocks are
+ * then sharded across ranks (64-block chunks dealt round-robin by zeta
+ * position); X and y are replicated on every rank; the only collective of
+ * the path is one ncclAllGather of the per-chunk partial sums (Alg.1
+ * Step 5), which keeps ell bit-identical for every world size. */
+int sbv_comm_unique_id(void *id128);
+int sbv_comm_init(sbv_handle h, const void *nccl_unique_id, int32_t rank, int32_t world);
+
+/* ---------------------------------------------------------------- prepare */
+
+/* Alg.1 Steps 1-3 on device:
+ *   H1  S = X / scale (IEEE division per element; Alg.2, Eq.5)
+ *   H2  k = max(1, floor(n/bs + 1/2)) anchors = the k points with smallest
+ *       (splitmix64(seed, i), i); anchor rank r seeds block r whose zeta
+ *       position is r (Alg.3, Alg.1; Q8, Q9)
+ *   H3  RAC: every point joins the block of its nearest anchor in scaled
+ *       space, ties to the lowest rank (Alg.3)
+ *   H4  block-major layout, members in ascending original index
+ *   H5  centroids = member means in scaled space (Alg.4)
+ *   H6  exact m-NN of each block centroid among the points of strictly
+ *       earlier blocks, ordered by (squared distance, original index)
+ *       (Eq.2, Alg.4; Q5, Q6, Q13)
+ * X: n x d (host or device).  scale: host double[d], every entry > 0.
+ * Requires 1 <= d <= SBV_MAX_D, 1 <= bs <= n, 0 <= m, n < 2^31, finite X.
+ * Errors: SBV_ERR_ARG, SBV_ERR_OOM, SBV_ERR_CUDA, SBV_ERR_COMM. */
+int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t bs,
+                  int32_t m, const double *scale);
+
+/* Convenience: sbv_create(opts) + sbv_prepare_h.  On error *out is NULL. */
+int sbv_prepare_ex(const double *X, int64_t n, int32_t d, int32_t bs, int32_t m,
+                   const double *scale, const sbv_opts *opts, sbv_handle *out);
+
+/* North-star form: sbv_prepare(X, n, d, bs, m, scale) with default options. */
+int sbv_prepare(const double *X, int64_t n, int32_t d, int32_t bs, int32_t m,
+                const double *scale, sbv_handle *out);
+
+/* ---------------------------------------------------------------- loglik */
+
+/* Alg.1 Steps 4-5: ell(theta; y) = sum_t ell_t with, per block t (Alg.5):
+ *   ell_t = -1/2 (v^T v + 2 sum_j log L'_jj) - (bs_t/2) log 2 pi
+ * where L' = chol(Sigma_lk - Sigma'cross^T Sigma'cross) and
+ * v = L'^{-1}(y_B - mu) (Q1, Q2), computed as one bordered
+ * Cholesky of the joint (m_t + bs_t) covariance of [J_t; B_t].
+ * Covariance: Eq.5-6 with theta's beta on the ORIGINAL inputs (Q11) and the
+ * nugget tau2 on the diagonal only (Q3).
+ * y: length n in original point order (host or device).
+ * theta: host double[d+3] = {sigma2, beta_1..beta_d, nu, tau2}.
+ * *ll receives ell (NaN on SBV_ERR_NOT_PD).  Synchronous on the stream.
+ * Errors: SBV_ERR_ARG (theta invalid), SBV_ERR_UNSUPPORTED (nu),
+ * SBV_ERR_NOT_PD (lowest failing zeta block + stage via sbv_last_error),
+ * SBV_ERR_STATE (no prepare), SBV_ERR_CUDA, SBV_ERR_COMM. */
+int sbv_loglik(sbv_handle h, const double *y, const double *theta, double *ll);
+
+/* As sbv_loglik, plus parts[0..3] = {ell, sum quad, sum logdet, #points}
+ * (host double[4], may be NULL). */
+int sbv_loglik_parts(sbv_handle h, const double *y, const double *theta, double *parts);
+
+/* Per-block terms ell_t (double[bc], zeta order; host or device).  Blocks
+ * owned by other ranks are written as NaN.  quad/logdet may be NULL. */
+int sbv_block_terms(sbv_handle h, const double *y, const double *theta, double *terms,
+                    double *quad, double *logdet);
+
+/* ---------------------------------------------------------------- introspection */
+
+int sbv_num_blocks(sbv_handle h, int64_t *bc);
+
+/* anchors: int32[bc] original index of the anchor of block r (host or device). */
+int sbv_get_anchors(sbv_handle h, int32_t *anchors);
+
+/* block_of_point: int32[n]; off: int64[bc+1] (block t = perm[off[t]..off[t+1]));
+ * perm: int32[n] original indices block-major; centroids: double[bc*d].
+ * Any output may be NULL. */
+int sbv_get_blocks(sbv_handle h, int32_t *block_of_point, int64_t *off, int32_t *perm,
+                   double *centroids);
+
+/* nbr: int32[bc*m] ORIGINAL point indices in kNN order, -1 padded; cnt:
+ * int32[bc].  Rows of blocks owned by other ranks are all -1 / count -1. */
+int sbv_get_neighbors(sbv_handle h, int32_t *nbr, int32_t *cnt);
+
+/* Realised-size statistics of the prepared handle (this rank's blocks):
+ * out[0] = algorithmic FP64 flops of one sbv_loglik (SURVEY 8(d) model,
+ *          LAPACK conventions, summed over the realised (m_t, bs_t)),
+ * out[1] = covariance entries generated per eval,
+ * out[2] = max N_t = m_t + bs_t, out[3] = min bs_t, out[4] = max bs_t,
+ * out[5] = number of local blocks, out[6] = kNN candidate pairs of prepare,
+ * out[7] = RAC pairs of prepare, out[8] = algorithmic HBM bytes of one
+ *          H8 launch (coordinates + y gathered + terms written). */
+int sbv_stats(sbv_handle h, double *out9);
+
+/* Per-stage device times (ms, CUDA events on the handle's stream) of the
+ * last sbv_prepare_h (prep=1) or sbv_loglik (prep=0) when opts.profile=1.
+ * names: static strings.  Returns the count in *count (<= cap). */
+int sbv_stage_times(sbv_handle h, int32_t prep, double *ms, const char **names, int32_t cap,
+                    int32_t *count);
+
+/* Last error of the handle: lowest failing zeta block (or -1), stage
+ * (1 = Sigma_con / neighbour part, 2 = Sigma_new / block part, 0 = none)
+ * and a static-lifetime message (valid until the next call on h). */
+int sbv_last_error(sbv_handle h, int64_t *block, int32_t *stage, const char **msg);
+
+int sbv_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SBV_H_ */

@@ -1,0 +1,606 @@
+// sbv_api.cu — the extern "C" boundary of libsbv (include/sbv.h).
+//
+// Orchestrates the device steps of Alg.1: sbv_prepare_h runs
+// Steps 1-3 (H1-H6, prep_kernels.cu) and sbv_loglik runs Steps 4-5 (H7-H10,
+// llh_kernel.cu).  No host arithmetic of the method happens here: the host
+// only validates arguments, sizes buffers, builds the block shard / work
+// order from the device-computed layout, and launches.
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <numeric>
+
+#include "sbv_internal.cuh"
+
+using namespace sbv;
+
+struct sbv_ctx : public Ctx {};
+
+namespace {
+
+int fail(sbv_ctx *h, int code, const char *msg) {
+  if (h) {
+    h->err_msg = msg;
+  }
+  return code;
+}
+
+#define CU(call)                                                        \
+  do {                                                                  \
+    cudaError_t e__ = (call);                                           \
+    if (e__ != cudaSuccess) {                                           \
+      if (h) h->err_msg = std::string(#call) + ": " + cudaGetErrorString(e__); \
+      return e__ == cudaErrorMemoryAllocation ? SBV_ERR_OOM : SBV_ERR_CUDA; \
+    }                                                                   \
+  } while (0)
+
+#define NC(call)                                                        \
+  do {                                                                  \
+    ncclResult_t r__ = (call);                                          \
+    if (r__ != ncclSuccess) {                                           \
+      if (h) h->err_msg = std::string(#call) + ": " + ncclGetErrorString(r__); \
+      return SBV_ERR_COMM;                                              \
+    }                                                                   \
+  } while (0)
+
+bool is_device_ptr(const void *p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+template <class T>
+cudaError_t ensure(T *&p, size_t count, size_t &cap_bytes_unused) {
+  (void)cap_bytes_unused;
+  if (p) cudaFree(p);
+  p = nullptr;
+  if (count == 0) count = 1;
+  return cudaMalloc(&p, count * sizeof(T));
+}
+
+template <class T>
+void release(T *&p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+void free_state(sbv_ctx *h) {
+  release(h->X);
+  release(h->S);
+  release(h->Sperm);
+  release(h->anchors);
+  release(h->block_of);
+  release(h->perm);
+  release(h->off);
+  release(h->C);
+  release(h->nbr);
+  release(h->cnt);
+  release(h->local_blocks);
+  release(h->work_order);
+  release(h->Xperm);
+  release(h->yperm);
+  release(h->ybuf);
+  release(h->terms);
+  release(h->quads);
+  release(h->logdets);
+  release(h->status);
+  release(h->chunk_local);
+  release(h->chunk_all);
+  release(h->result);
+  release(h->queue);
+  release(h->ws);
+  h->prepared = false;
+}
+
+__global__ void k_check_finite(const double *x, int64_t n, int *bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(x[i])) *bad = 1;
+}
+
+__global__ void k_scatter_terms(const double *src, const int32_t *local_blocks, int64_t k_local,
+                                double *dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k_local;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[local_blocks[i]] = src[i];
+}
+
+__global__ void k_fill_d(double *p, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void k_fill_i(int32_t *p, int64_t n, int32_t v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void k_nbr_to_orig(const int32_t *nbr, const int32_t *cnt, const int32_t *perm,
+                              const int32_t *local_blocks, int64_t k_local, int m,
+                              int32_t *out_nbr, int32_t *out_cnt) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < k_local * m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t li = e / m;
+    int j = (int)(e - li * m);
+    int64_t t = local_blocks[li];
+    int32_t p = nbr[e];
+    out_nbr[t * m + j] = (j < cnt[li] && p >= 0) ? perm[p] : -1;
+    if (j == 0) out_cnt[t] = cnt[li];
+  }
+  if (m == 0)
+    for (int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; li < k_local;
+         li += (int64_t)gridDim.x * blockDim.x)
+      out_cnt[local_blocks[li]] = 0;
+}
+
+__global__ void k_block_of_from_layout(const int32_t *perm, const int64_t *off, int64_t k,
+                                       int32_t *bo) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < k;
+       t += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t p = off[t]; p < off[t + 1]; p++) bo[perm[p]] = (int32_t)t;
+}
+
+int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); }
+
+// copy device array to a caller buffer that may be host or device
+int copy_out(sbv_ctx *h, void *dst, const void *src, size_t bytes) {
+  if (!dst || bytes == 0) return SBV_OK;
+  CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  return SBV_OK;
+}
+
+struct Timer {
+  sbv_ctx *h;
+  int prep;
+  int idx = 0;
+  Timer(sbv_ctx *h_, int prep_) : h(h_), prep(prep_) {
+    if (h->profile) cudaEventRecord(h->ev[0], h->stream);
+  }
+  void mark(const char *name) {
+    if (!h->profile || idx >= kMaxStages) return;
+    cudaEventRecord(h->ev[idx + 1], h->stream);
+    (prep ? h->name_prep : h->name_llh)[idx] = name;
+    idx++;
+  }
+  void finish() {
+    if (!h->profile) return;
+    cudaEventSynchronize(h->ev[idx]);
+    for (int i = 0; i < idx; i++) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, h->ev[i], h->ev[i + 1]);
+      (prep ? h->t_prep : h->t_llh)[i] = ms;
+    }
+    (prep ? h->n_ev_prep : h->n_ev_llh) = idx;
+  }
+};
+
+int validate_theta(sbv_ctx *h, const double *theta) {
+  if (!theta) return fail(h, SBV_ERR_ARG, "theta is NULL");
+  const int d = h->d;
+  for (int i = 0; i < d + 3; i++)
+    if (!isfinite(theta[i])) return fail(h, SBV_ERR_ARG, "theta has a non-finite entry");
+  if (!(theta[0] > 0)) return fail(h, SBV_ERR_ARG, "sigma2 must be > 0");
+  for (int j = 0; j < d; j++)
+    if (!(theta[1 + j] > 0)) return fail(h, SBV_ERR_ARG, "beta_j must be > 0");
+  if (!(theta[d + 2] >= 0)) return fail(h, SBV_ERR_ARG, "tau2 must be >= 0");
+  const double nu = theta[d + 1];
+  if (nu != 0.5 && nu != 1.5 && nu != 2.5 && nu != 3.5)
+    return fail(h, SBV_ERR_UNSUPPORTED, "nu must be one of 0.5, 1.5, 2.5, 3.5");
+  return SBV_OK;
+}
+
+// Steps 4-5 for the current handle; leaves per-block outputs on device and
+// the reduced vector in h->result_host.
+int run_loglik(sbv_ctx *h, const double *y, const double *theta) {
+  if (!h->prepared) return fail(h, SBV_ERR_STATE, "sbv_loglik before sbv_prepare");
+  if (!y) return fail(h, SBV_ERR_ARG, "y is NULL");
+  int rc = validate_theta(h, theta);
+  if (rc) return rc;
+  CU(cudaSetDevice(h->device));
+  Timer tm(h, 0);
+  const double *yd = y;
+  if (!is_device_ptr(y)) {
+    CU(cudaMemcpyAsync(h->ybuf, y, h->n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    yd = h->ybuf;
+  }
+  tm.mark("h2d_y");
+  CU(launch_stage_eval(yd, h->perm, h->n, h->yperm, h->stream));
+  tm.mark("H7_stage");
+  CU(launch_h8(*h, theta, h->stream));
+  tm.mark("H8_block_llh");
+  CU(launch_reduce_chunks(*h, h->stream));
+  tm.mark("H9_chunk_sums");
+  if (h->world > 1) {
+    int64_t ncl_pad = (h->n_chunks + h->world - 1) / h->world;
+    NC(ncclAllGather(h->chunk_local, h->chunk_all, (size_t)ncl_pad * 8, ncclDouble, h->comm,
+                     h->stream));
+    tm.mark("H10_allgather");
+  }
+  CU(launch_final_reduce(*h, h->stream));
+  CU(cudaMemcpyAsync(h->result_host, h->result, 8 * sizeof(double), cudaMemcpyDeviceToHost,
+                     h->stream));
+  tm.mark("H9_final_d2h");
+  CU(cudaStreamSynchronize(h->stream));
+  tm.finish();
+  if (h->result_host[4] > 0) {
+    h->err_block = (int64_t)h->result_host[5];
+    h->err_stage = (int32_t)h->result_host[6];
+    h->err_msg = "Cholesky factorisation failed (non-positive pivot)";
+    return SBV_ERR_NOT_PD;
+  }
+  h->err_block = -1;
+  h->err_stage = 0;
+  return SBV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sbv_abi_version(void) { return SBV_ABI_VERSION; }
+
+int sbv_create(const sbv_opts *opts, sbv_handle *out) {
+  if (!out) return SBV_ERR_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return SBV_ERR_CUDA;
+  }
+  sbv_ctx *h = new sbv_ctx();
+  cudaGetDevice(&h->device);
+  if (opts) {
+    h->seed = opts->seed;
+    h->stream = (cudaStream_t)opts->stream;
+    h->profile = opts->profile;
+  }
+  for (int i = 0; i <= kMaxStages; i++) cudaEventCreate(&h->ev[i]);
+  if (cudaMallocHost(&h->result_host, 8 * sizeof(double)) != cudaSuccess) {
+    delete h;
+    return SBV_ERR_OOM;
+  }
+  *out = h;
+  return SBV_OK;
+}
+
+void sbv_destroy(sbv_handle h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->stream);
+  free_state(h);
+  if (h->comm) ncclCommDestroy(h->comm);
+  for (int i = 0; i <= kMaxStages; i++)
+    if (h->ev[i]) cudaEventDestroy(h->ev[i]);
+  if (h->result_host) cudaFreeHost(h->result_host);
+  delete h;
+}
+
+int sbv_comm_unique_id(void *id128) {
+  if (!id128) return SBV_ERR_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return SBV_ERR_COMM;
+  memcpy(id128, &id, sizeof(id));
+  return SBV_OK;
+}
+
+int sbv_comm_init(sbv_handle h, const void *nccl_unique_id, int32_t rank, int32_t world) {
+  if (!h || !nccl_unique_id || world < 1 || rank < 0 || rank >= world) return SBV_ERR_ARG;
+  if (h->prepared) return fail(h, SBV_ERR_STATE, "sbv_comm_init must precede sbv_prepare_h");
+  if (world == 1) {
+    h->rank = 0;
+    h->world = 1;
+    return SBV_OK;
+  }
+  CU(cudaSetDevice(h->device));
+  ncclUniqueId id;
+  memcpy(&id, nccl_unique_id, sizeof(id));
+  if (h->comm) ncclCommDestroy(h->comm);
+  h->comm = nullptr;
+  NC(ncclCommInitRank(&h->comm, world, id, rank));
+  h->rank = rank;
+  h->world = world;
+  return SBV_OK;
+}
+
+int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t bs, int32_t m,
+                  const double *scale) {
+  if (!h) return SBV_ERR_ARG;
+  if (!X || !scale) return fail(h, SBV_ERR_ARG, "X or scale is NULL");
+  if (n < 1 || n >= (int64_t(1) << 31)) return fail(h, SBV_ERR_ARG, "n out of range");
+  if (d < 1 || d > SBV_MAX_D) return fail(h, SBV_ERR_ARG, "d out of range [1, 64]");
+  if (bs < 1 || bs > n) return fail(h, SBV_ERR_ARG, "bs out of range [1, n]");
+  if (m < 0) return fail(h, SBV_ERR_ARG, "m must be >= 0");
+  if (m > 1536) return fail(h, SBV_ERR_UNSUPPORTED, "m > 1536 not supported by the kNN kernel");
+  for (int j = 0; j < d; j++)
+    if (!(scale[j] > 0) || !isfinite(scale[j])) return fail(h, SBV_ERR_ARG, "scale_j must be finite and > 0");
+  CU(cudaSetDevice(h->device));
+  free_state(h);
+  h->n = n;
+  h->d = d;
+  h->bs = bs;
+  h->m = m;
+  h->scale.assign(scale, scale + d);
+  const int64_t k = std::max<int64_t>(1, (2 * n + bs) / (2 * (int64_t)bs));  // round(n/bs)
+  h->k = k;
+  cudaStream_t st = h->stream;
+  size_t unused = 0;
+  Timer tm(h, 1);
+
+  CU(ensure(h->X, n * d, unused));
+  CU(cudaMemcpyAsync(h->X, X, n * d * sizeof(double), cudaMemcpyDefault, st));
+  {
+    int *bad = nullptr;
+    CU(cudaMallocAsync(&bad, sizeof(int), st));
+    CU(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    k_check_finite<<<grid_for(n * d), 256, 0, st>>>(h->X, n * d, bad);
+    int hb = 0;
+    CU(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    cudaFreeAsync(bad, st);
+    if (hb) return fail(h, SBV_ERR_ARG, "X has non-finite entries");
+  }
+  tm.mark("h2d_X");
+  CU(ensure(h->S, n * d, unused));
+  CU(launch_scale(h->X, n, d, scale, h->S, st));
+  tm.mark("H1_scale");
+  CU(ensure(h->anchors, k, unused));
+  CU(select_anchors(n, k, h->seed, h->anchors, nullptr, 0, st, nullptr));
+  tm.mark("H2_anchors");
+  CU(ensure(h->block_of, n, unused));
+  CU(launch_rac(h->S, n, d, h->anchors, k, h->block_of, st));
+  tm.mark("H3_rac");
+  CU(ensure(h->perm, n, unused));
+  CU(ensure(h->off, k + 1, unused));
+  CU(build_layout(h->block_of, n, k, h->perm, h->off, nullptr, 0, st, nullptr));
+  CU(ensure(h->Sperm, n * d, unused));
+  CU(launch_gather_rows(h->S, h->perm, n, d, h->Sperm, st));
+  tm.mark("H4_layout");
+  CU(ensure(h->C, k * d, unused));
+  CU(launch_centroids(h->Sperm, h->off, k, d, h->C, st));
+  tm.mark("H5_centroids");
+
+  // shard: 64-block chunks of zeta order dealt round-robin over ranks
+  std::vector<int64_t> off_h(k + 1);
+  CU(cudaMemcpyAsync(off_h.data(), h->off, (k + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  h->n_chunks = (k + kChunkBlocks - 1) / kChunkBlocks;
+  std::vector<int32_t> local;
+  local.reserve(k / h->world + kChunkBlocks);
+  for (int64_t c = h->rank; c < h->n_chunks; c += h->world)
+    for (int64_t t = c * kChunkBlocks; t < std::min<int64_t>(k, (c + 1) * kChunkBlocks); t++)
+      local.push_back((int32_t)t);
+  h->k_local = (int64_t)local.size();
+  h->n_chunks_local = (h->k_local + kChunkBlocks - 1) / kChunkBlocks;
+  CU(ensure(h->local_blocks, h->k_local, unused));
+  CU(cudaMemcpyAsync(h->local_blocks, local.data(), h->k_local * sizeof(int32_t),
+                     cudaMemcpyHostToDevice, st));
+
+  const int mm = m > 0 ? m : 1;
+  CU(ensure(h->nbr, h->k_local * mm, unused));
+  CU(ensure(h->cnt, h->k_local, unused));
+  CU(launch_knn(h->Sperm, h->perm, h->off, h->C, h->local_blocks, h->k_local, d, m, h->nbr,
+                h->cnt, st));
+  tm.mark("H6_knn");
+
+  // realised sizes -> LPT work order, statistics, H8 launch geometry
+  std::vector<int32_t> cnt_h(h->k_local);
+  CU(cudaMemcpyAsync(cnt_h.data(), h->cnt, h->k_local * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  std::vector<int32_t> Nt(h->k_local);
+  h->max_N = 0;
+  h->min_bs = INT32_MAX;
+  h->max_bs = 0;
+  h->flops = h->entries = h->knn_pairs = 0;
+  for (int64_t li = 0; li < h->k_local; li++) {
+    int64_t t = local[li];
+    double b = (double)(off_h[t + 1] - off_h[t]), mt = cnt_h[li];
+    Nt[li] = (int32_t)(mt + b);
+    h->max_N = std::max(h->max_N, Nt[li]);
+    h->min_bs = std::min(h->min_bs, (int32_t)b);
+    h->max_bs = std::max(h->max_bs, (int32_t)b);
+    // SURVEY 8(d) flop model (LAPACK conventions)
+    h->flops += (mt * mt * mt / 3 + mt * mt / 2 + mt / 6) + mt * mt * b + mt * mt +
+                b * (b + 1) * mt + 2 * mt * b + (b * b * b / 3 + b * b / 2 + b / 6) + b * b + 2 * b;
+    h->entries += mt * (mt + 1) / 2 + mt * b + b * (b + 1) / 2;
+    h->knn_pairs += (double)off_h[t];
+  }
+  h->rac_pairs = (double)n * (double)k;
+  h->h8_bytes = 0;
+  for (int64_t li = 0; li < h->k_local; li++)
+    h->h8_bytes += (double)Nt[li] * (d + 1) * 8.0 + (double)cnt_h[li] * 4.0 + 4 * 8.0;
+  std::vector<int32_t> order(h->k_local);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return Nt[a] > Nt[b]; });
+  CU(ensure(h->work_order, h->k_local, unused));
+  CU(cudaMemcpyAsync(h->work_order, order.data(), h->k_local * sizeof(int32_t),
+                     cudaMemcpyHostToDevice, st));
+
+  // per-eval buffers
+  CU(ensure(h->Xperm, n * d, unused));
+  CU(launch_gather_rows(h->X, h->perm, n, d, h->Xperm, st));
+  CU(ensure(h->yperm, n, unused));
+  CU(ensure(h->ybuf, n, unused));
+  CU(ensure(h->terms, h->k_local, unused));
+  CU(ensure(h->quads, h->k_local, unused));
+  CU(ensure(h->logdets, h->k_local, unused));
+  CU(ensure(h->status, h->k_local, unused));
+  const int64_t ncl_pad = h->world > 1 ? (h->n_chunks + h->world - 1) / h->world : h->n_chunks;
+  CU(ensure(h->chunk_local, std::max<int64_t>(ncl_pad, 1) * 8, unused));
+  CU(cudaMemsetAsync(h->chunk_local, 0, std::max<int64_t>(ncl_pad, 1) * 8 * sizeof(double), st));
+  if (h->world > 1) CU(ensure(h->chunk_all, (int64_t)h->world * ncl_pad * 8, unused));
+  CU(ensure(h->result, 8, unused));
+  CU(ensure(h->queue, 1, unused));
+  int sms = 0;
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+  h->h8_smem = h8_smem_bytes(std::max(h->max_N, 1), d);
+  int smem_optin = 0;
+  CU(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+  if (h->h8_smem + 1024 > (size_t)smem_optin)
+    return fail(h, SBV_ERR_UNSUPPORTED, "block + neighbour set too large for shared memory staging");
+  int per_sm = h8_max_ctas_per_sm(h->h8_smem);
+  if (per_sm < 1) per_sm = 1;
+  h->h8_grid = (int)std::min<int64_t>((int64_t)sms * per_sm, std::max<int64_t>(h->k_local, 1));
+  h->ws_per_cta = h8_ws_doubles(std::max(h->max_N, 1));
+  CU(ensure(h->ws, (size_t)h->h8_grid * h->ws_per_cta, unused));
+  CU(cudaStreamSynchronize(st));
+  tm.mark("meta");
+  tm.finish();
+  h->prepared = true;
+  return SBV_OK;
+}
+
+int sbv_prepare_ex(const double *X, int64_t n, int32_t d, int32_t bs, int32_t m,
+                   const double *scale, const sbv_opts *opts, sbv_handle *out) {
+  if (!out) return SBV_ERR_ARG;
+  *out = nullptr;
+  sbv_handle h = nullptr;
+  int rc = sbv_create(opts, &h);
+  if (rc) return rc;
+  rc = sbv_prepare_h(h, X, n, d, bs, m, scale);
+  if (rc) {
+    sbv_destroy(h);
+    return rc;
+  }
+  *out = h;
+  return SBV_OK;
+}
+
+int sbv_prepare(const double *X, int64_t n, int32_t d, int32_t bs, int32_t m, const double *scale,
+                sbv_handle *out) {
+  return sbv_prepare_ex(X, n, d, bs, m, scale, nullptr, out);
+}
+
+int sbv_loglik_parts(sbv_handle h, const double *y, const double *theta, double *parts) {
+  if (!h) return SBV_ERR_ARG;
+  int rc = run_loglik(h, y, theta);
+  const double two_pi_half = 0.91893853320467274178;  // log(2 pi) / 2
+  (void)two_pi_half;
+  if (parts) {
+    parts[0] = rc == SBV_OK ? h->result_host[0] : NAN;
+    parts[1] = h->result_host[1];
+    parts[2] = h->result_host[2];
+    parts[3] = h->result_host[3];
+  }
+  return rc;
+}
+
+int sbv_loglik(sbv_handle h, const double *y, const double *theta, double *ll) {
+  if (!h) return SBV_ERR_ARG;
+  if (!ll) return fail(h, SBV_ERR_ARG, "ll is NULL");
+  int rc = run_loglik(h, y, theta);
+  *ll = rc == SBV_OK ? h->result_host[0] : NAN;
+  return rc;
+}
+
+int sbv_block_terms(sbv_handle h, const double *y, const double *theta, double *terms,
+                    double *quad, double *logdet) {
+  if (!h) return SBV_ERR_ARG;
+  int rc = run_loglik(h, y, theta);
+  if (rc != SBV_OK && rc != SBV_ERR_NOT_PD) return rc;
+  double *tmp = nullptr;
+  cudaStream_t st = h->stream;
+  CU(cudaMallocAsync(&tmp, h->k * sizeof(double), st));
+  const double *srcs[3] = {h->terms, h->quads, h->logdets};
+  double *dsts[3] = {terms, quad, logdet};
+  for (int i = 0; i < 3; i++) {
+    if (!dsts[i]) continue;
+    k_fill_d<<<grid_for(h->k), 256, 0, st>>>(tmp, h->k, NAN);
+    k_scatter_terms<<<grid_for(h->k_local), 256, 0, st>>>(srcs[i], h->local_blocks, h->k_local, tmp);
+    int r2 = copy_out(h, dsts[i], tmp, h->k * sizeof(double));
+    if (r2) return r2;
+  }
+  cudaFreeAsync(tmp, st);
+  CU(cudaStreamSynchronize(st));
+  return rc;
+}
+
+int sbv_num_blocks(sbv_handle h, int64_t *bc) {
+  if (!h || !bc) return SBV_ERR_ARG;
+  if (!h->prepared) return fail(h, SBV_ERR_STATE, "not prepared");
+  *bc = h->k;
+  return SBV_OK;
+}
+
+int sbv_get_anchors(sbv_handle h, int32_t *anchors) {
+  if (!h || !anchors) return SBV_ERR_ARG;
+  if (!h->prepared) return fail(h, SBV_ERR_STATE, "not prepared");
+  return copy_out(h, anchors, h->anchors, h->k * sizeof(int32_t));
+}
+
+int sbv_get_blocks(sbv_handle h, int32_t *block_of_point, int64_t *off, int32_t *perm,
+                   double *centroids) {
+  if (!h) return SBV_ERR_ARG;
+  if (!h->prepared) return fail(h, SBV_ERR_STATE, "not prepared");
+  int rc;
+  if ((rc = copy_out(h, block_of_point, h->block_of, h->n * sizeof(int32_t)))) return rc;
+  if ((rc = copy_out(h, off, h->off, (h->k + 1) * sizeof(int64_t)))) return rc;
+  if ((rc = copy_out(h, perm, h->perm, h->n * sizeof(int32_t)))) return rc;
+  if ((rc = copy_out(h, centroids, h->C, h->k * h->d * sizeof(double)))) return rc;
+  return SBV_OK;
+}
+
+int sbv_get_neighbors(sbv_handle h, int32_t *nbr, int32_t *cnt) {
+  if (!h) return SBV_ERR_ARG;
+  if (!h->prepared) return fail(h, SBV_ERR_STATE, "not prepared");
+  cudaStream_t st = h->stream;
+  const int m = h->m;
+  int32_t *tn = nullptr, *tc = nullptr;
+  CU(cudaMallocAsync(&tn, std::max<int64_t>(h->k * m, 1) * sizeof(int32_t), st));
+  CU(cudaMallocAsync(&tc, h->k * sizeof(int32_t), st));
+  k_fill_i<<<grid_for(h->k * m), 256, 0, st>>>(tn, h->k * m, -1);
+  k_fill_i<<<grid_for(h->k), 256, 0, st>>>(tc, h->k, -1);
+  k_nbr_to_orig<<<grid_for(std::max<int64_t>(h->k_local * m, h->k_local)), 256, 0, st>>>(
+      h->nbr, h->cnt, h->perm, h->local_blocks, h->k_local, m, tn, tc);
+  int rc = SBV_OK;
+  if (nbr && m > 0) rc = copy_out(h, nbr, tn, h->k * m * sizeof(int32_t));
+  if (!rc && cnt) rc = copy_out(h, cnt, tc, h->k * sizeof(int32_t));
+  cudaFreeAsync(tn, st);
+  cudaFreeAsync(tc, st);
+  CU(cudaStreamSynchronize(st));
+  return rc;
+}
+
+int sbv_stats(sbv_handle h, double *out9) {
+  if (!h || !out9) return SBV_ERR_ARG;
+  if (!h->prepared) return fail(h, SBV_ERR_STATE, "not prepared");
+  out9[0] = h->flops;
+  out9[1] = h->entries;
+  out9[2] = h->max_N;
+  out9[3] = h->min_bs;
+  out9[4] = h->max_bs;
+  out9[5] = (double)h->k_local;
+  out9[6] = h->knn_pairs;
+  out9[7] = h->rac_pairs;
+  out9[8] = h->h8_bytes;
+  return SBV_OK;
+}
+
+int sbv_stage_times(sbv_handle h, int32_t prep, double *ms, const char **names, int32_t cap,
+                    int32_t *count) {
+  if (!h || !count) return SBV_ERR_ARG;
+  int nn = prep ? h->n_ev_prep : h->n_ev_llh;
+  nn = std::min(nn, (int)cap);
+  for (int i = 0; i < nn; i++) {
+    if (ms) ms[i] = prep ? h->t_prep[i] : h->t_llh[i];
+    if (names) names[i] = prep ? h->name_prep[i] : h->name_llh[i];
+  }
+  *count = nn;
+  return SBV_OK;
+}
+
+int sbv_last_error(sbv_handle h, int64_t *block, int32_t *stage, const char **msg) {
+  if (!h) return SBV_ERR_ARG;
+  if (block) *block = h->err_block;
+  if (stage) *stage = h->err_stage;
+  if (msg) *msg = h->err_msg.c_str();
+  return SBV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+// sbv_internal.cuh — shared declarations of libsbv's CUDA translation units.
+// Product path only; nothing here is shared with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/sbv.h"
+
+namespace sbv {
+
+constexpr int kPanel = 32;       // H8 panel width (columns per left-looking step)
+constexpr int kChunkBlocks = 64; // blocks per reduction / shard chunk
+constexpr int kMaxStages = 16;
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint64_t seed = 3;
+  int profile = 0;
+  // comm
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  // problem
+  bool prepared = false;
+  int64_t n = 0;
+  int32_t d = 0, bs = 0, m = 0;
+  int64_t k = 0;  // number of blocks bc
+  std::vector<double> scale;
+  // device state (prepare)
+  double *X = nullptr;        // n x d original inputs (library copy)
+  double *S = nullptr;        // n x d scaled by `scale` (original order)
+  double *Sperm = nullptr;    // n x d scaled, block-major
+  int32_t *anchors = nullptr; // k
+  int32_t *block_of = nullptr;// n
+  int32_t *perm = nullptr;    // n, block-major -> original index
+  int64_t *off = nullptr;     // k+1
+  double *C = nullptr;        // k x d centroids
+  int32_t *nbr = nullptr;     // k_local x m, positions in block-major order, -1 pad
+  int32_t *cnt = nullptr;     // k_local
+  int32_t *local_blocks = nullptr; // k_local zeta ids of this rank's blocks (ascending)
+  int32_t *work_order = nullptr;   // k_local indices into local_blocks, LPT order
+  int64_t k_local = 0;
+  int64_t n_chunks = 0, n_chunks_local = 0;
+  int32_t max_N = 0, min_bs = 0, max_bs = 0;
+  double flops = 0, entries = 0, knn_pairs = 0, rac_pairs = 0, h8_bytes = 0;
+  // per-eval buffers
+  double *Xperm = nullptr;    // n x d block-major ORIGINAL inputs (prepare)
+  double *yperm = nullptr;    // n block-major
+  double *ybuf = nullptr;     // n original order (host y staging)
+  double *terms = nullptr, *quads = nullptr, *logdets = nullptr; // k_local
+  int32_t *status = nullptr;  // k_local (0 ok, 1/2 failing stage)
+  double *chunk_local = nullptr;  // n_chunks_local_pad x 4
+  double *chunk_all = nullptr;    // world * n_chunks_local_pad x 4
+  double *result = nullptr;       // 8 doubles: ell, quad, logdet, npts, nfail, fail_block, fail_stage, -
+  double *result_host = nullptr;  // pinned 8 doubles
+  unsigned int *queue = nullptr;  // work counter
+  double *ws = nullptr;           // H8 per-CTA L workspaces
+  size_t ws_per_cta = 0;
+  int h8_grid = 0;
+  size_t h8_smem = 0;
+  // errors
+  int64_t err_block = -1;
+  int32_t err_stage = 0;
+  std::string err_msg;
+  // profiling
+  cudaEvent_t ev[kMaxStages + 1] = {};
+  int n_ev_prep = 0, n_ev_llh = 0;
+  double t_prep[kMaxStages] = {}, t_llh[kMaxStages] = {};
+  const char *name_prep[kMaxStages] = {}, *name_llh[kMaxStages] = {};
+};
+
+// ---- prepare kernels (prep_kernels.cu)
+cudaError_t launch_scale(const double *X, int64_t n, int d, const double *scale_host, double *S,
+                         cudaStream_t st);
+cudaError_t select_anchors(int64_t n, int64_t k, uint64_t seed, int32_t *anchors, void *tmp,
+                           size_t tmp_bytes, cudaStream_t st, size_t *tmp_needed);
+cudaError_t launch_rac(const double *S, int64_t n, int d, const int32_t *anchors, int64_t k,
+                       int32_t *block_of, cudaStream_t st);
+cudaError_t build_layout(const int32_t *block_of, int64_t n, int64_t k, int32_t *perm,
+                         int64_t *off, void *tmp, size_t tmp_bytes, cudaStream_t st,
+                         size_t *tmp_needed);
+cudaError_t launch_gather_rows(const double *S, const int32_t *perm, int64_t n, int d,
+                               double *Sperm, cudaStream_t st);
+cudaError_t launch_centroids(const double *Sperm, const int64_t *off, int64_t k, int d,
+                             double *C, cudaStream_t st);
+cudaError_t launch_knn(const double *Sperm, const int32_t *perm, const int64_t *off,
+                       const double *C, const int32_t *local_blocks, int64_t k_local, int d,
+                       int m, int32_t *nbr, int32_t *cnt, cudaStream_t st);
+
+// ---- per-eval kernels (llh_kernel.cu)
+cudaError_t launch_stage_eval(const double *y, const int32_t *perm, int64_t n, double *yperm,
+                              cudaStream_t st);
+size_t h8_smem_bytes(int max_N, int d);
+size_t h8_ws_doubles(int max_N);
+int h8_max_ctas_per_sm(size_t smem);
+cudaError_t launch_h8(const Ctx &c, const double *theta_host, cudaStream_t st);
+cudaError_t launch_reduce_chunks(const Ctx &c, cudaStream_t st);
+cudaError_t launch_final_reduce(const Ctx &c, cudaStream_t st);
+
+}  // namespace sbv

@@ -1,0 +1,187 @@
+"""GPU parity: libsbv (CUDA, through the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star): block/neighbour indices bit-exact, per-block
+terms within 1e-10 relative, the log-likelihood within 1e-9 relative
+(Q18 relative base).  Inputs are seeded and synthetic (sbv_inputs).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import sbv_inputs as si
+
+pytestmark = pytest.mark.gpu
+
+TOL_LL = 1e-9
+TOL_TERM = 1e-10
+
+
+@pytest.fixture(scope="module")
+def sbv():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2504_12004_b200 as p
+    from paper_2504_12004_b200 import build
+    build.build()
+    return p
+
+
+def run_both(sbv, orc, X, y, bs, m, scale, theta, seed=3, device=True):
+    import torch
+    Xt = torch.from_numpy(X).cuda() if device else X
+    yt = torch.from_numpy(y).cuda() if device else y
+    h = sbv.prepare(Xt, bs, m, scale, seed=seed)
+    P = orc.prepare(X, bs, m, scale, seed)
+    return h, P, Xt, yt
+
+
+def check_indices(h, P):
+    np.testing.assert_array_equal(h.anchors(), P["anchors"])
+    bo, off, perm, C = h.blocks()
+    np.testing.assert_array_equal(bo, P["block_of"])
+    np.testing.assert_array_equal(off, P["off"])
+    np.testing.assert_array_equal(perm, P["perm"])
+    np.testing.assert_array_equal(C, P["C"])  # bit-exact centroids (same summation order)
+    nbr, cnt = h.neighbors()
+    np.testing.assert_array_equal(cnt, P["cnt"])
+    np.testing.assert_array_equal(nbr, P["nbr"])
+
+
+def check_terms(h, orc, X, y, yt, P, theta):
+    ll_o, terms_o, quads_o, logdets_o = orc.loglik(X, y, P["perm"], P["off"], P["nbr"], P["cnt"],
+                                                    theta, return_terms=True)
+    terms, quads, logdets = h.block_terms(yt, theta)
+    # DESIGN.md Q18: relative to the term's own magnitude, guarded against
+    # cancellation between its parts (-1/2 quad, -1/2 logdet, -bs/2 log 2pi)
+    bsz = np.diff(P["off"])
+    base = np.maximum(np.abs(terms_o),
+                      0.5 * (np.abs(quads_o) + np.abs(logdets_o)) + 0.5 * bsz * math.log(2 * math.pi))
+    rel = np.abs(terms - terms_o) / base
+    assert rel.max() <= TOL_TERM, (rel.max(), int(rel.argmax()))
+    ll = h.loglik(yt, theta)
+    den = max(abs(ll_o), np.abs(terms_o).sum())
+    assert abs(ll - ll_o) <= TOL_LL * den, (ll, ll_o)
+    return ll, ll_o
+
+
+@pytest.mark.parametrize("d,bs,m,nu", [
+    (10, 20, 60, 2.5),   # cfg1 shape, reduced n
+    (10, 10, 30, 3.5),   # paper's nu, bs=10
+    (2, 7, 13, 0.5),
+    (5, 33, 90, 1.5),
+    (3, 1, 5, 2.5),      # bs = 1 (SV degenerate)
+    (10, 50, 0, 2.5),    # m = 0: marginal block terms only
+])
+def test_parity_small(sbv, orc, d, bs, m, nu):
+    n = 3000
+    X = si.make_X(n, d, seed=10 + d)
+    y = si.make_y(X, seed=20 + d)
+    scale = si.default_scale(d)
+    theta = si.default_theta(d, nu=nu, tau2=1e-4)
+    h, P, Xt, yt = run_both(sbv, orc, X, y, bs, m, scale, theta)
+    check_indices(h, P)
+    check_terms(h, orc, X, y, yt, P, theta)
+
+
+def test_parity_large_blocks_multi_pass(sbv, orc):
+    """N_t = m + bs up to ~700 rows: several 256-row passes per panel, ragged tails."""
+    n, d, bs, m = 4000, 4, 300, 350
+    X = si.make_X(n, d, seed=5)
+    y = si.make_y(X, seed=6)
+    scale = np.array([0.2, 0.3, 1.0, 2.0])
+    theta = np.array([1.3, 0.2, 0.3, 1.0, 2.0, 2.5, 1e-3])
+    h, P, Xt, yt = run_both(sbv, orc, X, y, bs, m, scale, theta)
+    check_indices(h, P)
+    check_terms(h, orc, X, y, yt, P, theta)
+    assert h.stats()["max_N"] > 600
+
+
+def test_parity_lattice_ties(sbv, orc):
+    """Exactly representable lattice data: massive distance ties exercise the
+    index tie rules of RAC (lowest anchor rank) and kNN (lowest index)."""
+    n, d = 2500, 3
+    X = si.make_X(n, d, seed=77, kind="lattice")
+    y = si.make_y(X, seed=78)
+    scale = np.array([0.5, 1.0, 2.0])
+    theta = np.array([1.0, 0.5, 1.0, 2.0, 2.5, 1e-2])
+    h, P, Xt, yt = run_both(sbv, orc, X, y, 12, 40, scale, theta)
+    check_indices(h, P)
+
+
+def test_full_conditioning_matches_dense_via_gpu(sbv, orc):
+    """m >= n: the GPU block-Vecchia likelihood equals the exact Eq.1 likelihood."""
+    from tests.test_oracle_pins import dense_loglik
+    import torch
+    n, d = 300, 10
+    X = si.make_X(n, d, seed=21)
+    y = si.make_y(X, seed=22, kind="iid")
+    theta = np.array([1.3, *np.linspace(0.8, 3.0, d), 2.5, 1e-3])
+    h = sbv.prepare(torch.from_numpy(X).cuda(), 10, n - 1, theta[1:1 + d])
+    ll = h.loglik(torch.from_numpy(y).cuda(), theta)
+    ref = dense_loglik(X, y, theta)
+    assert abs(ll - ref) <= 1e-9 * abs(ref)
+
+
+def test_host_and_device_pointers_agree(sbv, orc):
+    n, d = 1500, 6
+    X = si.make_X(n, d, seed=31)
+    y = si.make_y(X, seed=32)
+    theta = si.default_theta(d, nu=2.5)
+    import torch
+    h1 = sbv.prepare(X, 15, 40, si.default_scale(d))
+    h2 = sbv.prepare(torch.from_numpy(X).cuda(), 15, 40, si.default_scale(d))
+    a = h1.loglik(y, theta)
+    b = h2.loglik(torch.from_numpy(y).cuda(), theta)
+    assert a == b  # same kernels, same order: bitwise
+    assert h1.loglik(y, theta) == a  # repeatable
+
+
+def test_not_pd_reports_lowest_block_and_stage(sbv, orc):
+    X = si.make_X(400, 2, seed=81, kind="duplicates")
+    theta = np.array([1.0, 0.3, 0.3, 2.5, 0.0])
+    y = np.zeros(400)
+    h = sbv.prepare(X, 400, 0, theta[1:3])  # one block containing both copies
+    with pytest.raises(sbv.SBVError) as e:
+        h.loglik(y, theta)
+    assert e.value.code == 4 and e.value.block == 0 and e.value.stage == 2
+    # full conditioning: the later copy's conditioning set holds the earlier copy
+    P = orc.prepare(X, 1, 399, theta[1:3], 3)
+    with pytest.raises(orc.NotPD) as eo:
+        orc.loglik(X, y, P["perm"], P["off"], P["nbr"], P["cnt"], theta)
+    h = sbv.prepare(X, 1, 399, theta[1:3])
+    with pytest.raises(sbv.SBVError) as e:
+        h.loglik(y, theta)
+    assert e.value.block == eo.value.block and e.value.stage == eo.value.stage
+
+
+def test_argument_errors(sbv):
+    X = si.make_X(100, 3, seed=1)
+    with pytest.raises(sbv.SBVError) as e:
+        sbv.prepare(X, 0, 5, np.ones(3))
+    assert e.value.code == 1
+    with pytest.raises(sbv.SBVError):
+        sbv.prepare(X, 10, 5, np.array([1.0, -1.0, 1.0]))
+    Xn = X.copy()
+    Xn[3, 1] = np.nan
+    with pytest.raises(sbv.SBVError):
+        sbv.prepare(Xn, 10, 5, np.ones(3))
+    h = sbv.prepare(X, 10, 5, np.ones(3))
+    with pytest.raises(sbv.SBVError) as e:
+        h.loglik(np.zeros(100), np.array([1.0, 1, 1, 1, 1.0, 0.0]))  # nu = 1.0 unsupported
+    assert e.value.code == 5
+    with pytest.raises(sbv.SBVError) as e:
+        h.loglik(np.zeros(100), np.array([-1.0, 1, 1, 1, 2.5, 0.0]))
+    assert e.value.code == 1
+
+
+def test_cfg1_full_size(sbv, orc):
+    """BASELINE.json configs[0]: n=20,000, d=10, bs=20, m=60, Matérn-5/2."""
+    c = si.CONFIGS["cfg1"]
+    X = si.make_X(c["n"], c["d"], seed=1)
+    y = si.make_y(X, seed=2)
+    theta = si.default_theta(c["d"], nu=c["nu"], tau2=1e-4)
+    h, P, Xt, yt = run_both(sbv, orc, X, y, c["bs"], c["m"], si.default_scale(c["d"]), theta)
+    check_indices(h, P)
+    check_terms(h, orc, X, y, yt, P, theta)
