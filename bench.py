@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark of the SBV log-likelihood hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
+
+One STEP = one pass of the whole hot path over the
+synthetic workload: sbv_prepare_h (scale, RAC, zeta order, layout, centroids,
+kNN) + sbv_loglik (staging, fused per-block Cholesky kernel, reductions, and
+the NCCL exchange when N > 1), inputs resident in HBM.  Workload at N=1:
+BASELINE.json configs[1] (n=1M, d=10, bs=100, m=200, one eval on 1 B200).
+N > 1 (torchrun, one process per GPU) evaluates the SAME problem with blocks
+sharded across ranks (strong scaling).  Rank 0 prints one JSON line.
+
+--impl reference times the CPU oracle (oracle/, the "reference arm" for this
+tier) on the box's host cores on a bounded sample of the same workload and
+scales it to the same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import sbv_inputs as si  # noqa: E402
+
+METRIC = "Vecchia loglik evals/sec and FP64 TFLOP/s (% of peak) at 1/2/4/8 B200"
+FP64_PEAK_FALLBACK = 37.1  # TF/s, DMMA.8x8x4 microbenchmark on this pool (profiles/r01/fp64_peaks.jsonl)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peaks = {}
+    if os.path.exists(p):
+        peaks = json.load(open(p))
+    fp64 = None
+    f = os.path.join(ROOT, "profiles", "r01", "fp64_peaks.jsonl")
+    if os.path.exists(f):
+        for line in open(f):
+            try:
+                r = json.loads(line)
+            except Exception:
+                continue
+            if r.get("kind") == "dmma_8x8x4":
+                fp64 = max(fp64 or 0, r["tflops"])
+    return peaks, fp64 or FP64_PEAK_FALLBACK
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"bench_clocks_{gpu}.csv")
+
+    def start(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def workload(cfg: str):
+    c = dict(si.CONFIGS[cfg])
+    return c
+
+
+# ----------------------------------------------------------------------------- reference arm
+def oracle_sample(c, n_s: int, nthreads: int):
+    """Time the oracle (as it stands) on an n_s-point sample of the workload and
+    scale to one full eval with the path's complexity: prepare (RAC n*k + kNN
+    n*k/2 pair work) ~ n^2, loglik ~ number of blocks."""
+    import oracle
+    d, bs, m, nu = c["d"], c["bs"], c["m"], c["nu"]
+    X = si.make_X(n_s, d, seed=1)
+    y = si.make_y(X, seed=2, kind="iid")
+    theta = si.default_theta(d, nu=nu, tau2=1e-4)
+    scale = si.default_scale(d)
+    t0 = time.perf_counter()
+    P = oracle.prepare(X, bs, m, scale, 3, nthreads=nthreads)
+    t1 = time.perf_counter()
+    ll = oracle.loglik(X, y, P["perm"], P["off"], P["nbr"], P["cnt"], theta, nthreads=nthreads)
+    t2 = time.perf_counter()
+    r = c["n"] / n_s
+    t_full = (t1 - t0) * r * r + (t2 - t1) * r
+    return dict(t_prep=t1 - t0, t_llh=t2 - t1, t_full=t_full, ll=ll,
+                sample=f"oracle prepare+loglik on n={n_s} points of the {c['n']}-point workload "
+                       f"(same d/bs/m/theta), scaled to n={c['n']} as prepare*(n/n_s)^2 + loglik*(n/n_s)")
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    c = workload(args.config)
+    nthreads = os.cpu_count() or 1
+    n_s = args.ref_sample
+    for _ in range(args.warmup):
+        oracle_sample(c, n_s, nthreads)
+    times = []
+    last = None
+    for _ in range(args.steps):
+        last = oracle_sample(c, n_s, nthreads)
+        times.append(last["t_full"])
+    t = statistics.mean(times)
+    val = 1.0 / t
+    out = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "evals/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_dict(c, args.config, args.gpus),
+        "cpu_baseline": {"value": val, "unit": "evals/s", "cores": nthreads, "kind": "oracle",
+                         "sample": last["sample"]},
+        "e2e": {"value": val, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+    return 0
+
+
+def config_dict(c, name, ngpu):
+    return {"workload": f"{name}: n={c['n']} d={c['d']} bs={c['bs']} m={c['m']} nu={c['nu']} "
+                        f"Matern, X~U[0,1]^d, beta=(0.05,0.05,5x8), tau2=1e-4, y iid N(0,1)",
+            "n": c["n"], "d": c["d"], "bs": c["bs"], "m": c["m"], "nu": c["nu"],
+            "step": "sbv_prepare_h (H1-H6) + sbv_loglik (H7-H10)",
+            "parallelism": f"blocks sharded over {ngpu} GPU(s), X/y replicated",
+            "l2": "flushed between timed steps (256 MiB write) and step working set > L2"}
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_12004_b200 as sbv
+    from paper_2504_12004_b200 import build
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if rank == 0:
+        build.build()
+    if world > 1:
+        dist.barrier()
+    peaks, fp64_peak = load_peaks()
+    c = workload(args.config)
+    n, d, bs, m, nu = c["n"], c["d"], c["bs"], c["m"], c["nu"]
+    X_h = si.make_X(n, d, seed=1)
+    y_h = si.make_y(X_h, seed=2, kind="iid")
+    theta = si.default_theta(d, nu=nu, tau2=1e-4)
+    scale = si.default_scale(d)
+    X = torch.from_numpy(X_h).to(dev)
+    y = torch.from_numpy(y_h).to(dev)
+    stream = torch.cuda.current_stream(dev)
+
+    uid = None
+    if world > 1:
+        obj = [sbv.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+
+    h = sbv.Handle(seed=3, stream=stream, profile=True)
+    if world > 1:
+        h.comm_init(uid, rank, world)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        h.prepare(X, bs, m, scale)
+        return h.loglik(y, theta)
+
+    for _ in range(max(args.warmup, 0)):
+        ll = step()
+    stats = h.stats()
+    # --- timed region: K steps, CUDA events on the handle's stream, L2 flushed between steps
+    e0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    e1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    stage_prep, stage_llh = {}, {}
+    clocks = Clocks(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for i in range(args.steps):
+        flush.zero_()
+        e0[i].record(stream)
+        ll = step()
+        e1[i].record(stream)
+        for k_, v in h.stage_times(True).items():
+            stage_prep.setdefault(k_, []).append(v)
+        for k_, v in h.stage_times(False).items():
+            stage_llh.setdefault(k_, []).append(v)
+    torch.cuda.synchronize()
+    ck = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    ms = sum(a.elapsed_time(b) for a, b in zip(e0, e1)) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+
+    # --- loglik-only rate (the MLE inner loop with the prepared handle)
+    for _ in range(3):
+        h.loglik(y, theta)
+    torch.cuda.synchronize()
+    reps = max(args.steps, 5)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    llh_ms, h8_ms = [], []
+    for _ in range(reps):
+        flush.zero_()
+        a.record(stream)
+        h.loglik(y, theta)
+        b.record(stream)
+        torch.cuda.synchronize()
+        llh_ms.append(a.elapsed_time(b))
+        h8_ms.append(h.stage_times(False)["H8_block_llh"])
+    tl = torch.tensor([statistics.mean(llh_ms), statistics.mean(h8_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tl, op=dist.ReduceOp.MAX)
+    llh_ms_max, h8_ms_max = float(tl[0]), float(tl[1])
+    flops_local = torch.tensor([stats["flops"], stats["h8_bytes"]], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(flops_local)
+    flops_total, h8_bytes_total = float(flops_local[0]), float(flops_local[1])
+
+    # --- e2e through the public API with HOST buffers (H2D of X, y and D2H of the result inside)
+    X_pin = torch.from_numpy(X_h).pin_memory()
+    y_pin = torch.from_numpy(y_h).pin_memory()
+    he = sbv.Handle(seed=3, stream=stream)
+    if world > 1:
+        obj = [sbv.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        he.comm_init(obj[0], rank, world)
+    he.prepare(X_pin, bs, m, scale)
+    he.loglik(y_pin, theta)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e2e_ms = []
+    for _ in range(max(2, min(args.steps, 5))):
+        flush.zero_()
+        a.record(stream)
+        he.prepare(X_pin, bs, m, scale)
+        he.loglik(y_pin, theta)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    te = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms_max = float(te.item())
+
+    # --- kernel launches in one step (CUPTI via torch.profiler, outside the timed region)
+    launches = None
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step()
+            torch.cuda.synchronize()
+        launches = sum(1 for ev in prof.events() if ev.device_type.name == "CUDA"
+                       and ("sbv" in ev.name or "cub" in ev.name.lower()))
+    except Exception:
+        launches = None
+
+    if rank == 0:
+        evals_s = 1e3 / ms_max
+        prep_mean = {k_: statistics.mean(v) for k_, v in stage_prep.items()}
+        llh_mean = {k_: statistics.mean(v) for k_, v in stage_llh.items()}
+        stages = {**{"prep." + k_: v for k_, v in prep_mean.items()},
+                  **{"llh." + k_: v for k_, v in llh_mean.items()}}
+        dom = max(((k_, v) for k_, v in stages.items() if "H" in k_), key=lambda kv: kv[1])
+        h8_tf = flops_total / (h8_ms_max * 1e-3) / 1e12
+        roof = roofline(dom, stats, c, fp64_peak, peaks, world, h8_ms_max, flops_total, h8_bytes_total)
+        out = {
+            "metric": METRIC, "value": evals_s, "unit": "evals/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_dict(c, args.config, world),
+            "tflops_step": flops_total / (ms_max * 1e-3) / 1e12,
+            "loglik_only": {"evals_s": 1e3 / llh_ms_max, "ms": llh_ms_max,
+                            "tflops": flops_total / (llh_ms_max * 1e-3) / 1e12,
+                            "h8_ms": h8_ms_max, "h8_tflops": h8_tf,
+                            "h8_frac_of_fp64_peak": h8_tf / fp64_peak,
+                            "fp64_peak_tflops": fp64_peak, "flops_per_eval": flops_total},
+            "stage_ms_rank0": stages,
+            "dominant_stage": dom[0],
+            "roofline": roof,
+            "e2e": {"value": 1e3 / e2e_ms_max, "unit": "evals/s",
+                    "h2d_bytes_per_step": int(n * d * 8 + n * 8), "d2h_bytes_per_step": 8 * 8},
+            "gpu_launches": launches,
+            "clocks": ck,
+            "ll": ll,
+            "realised": stats,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            import oracle
+            oracle.build()
+            nth = os.cpu_count() or 1
+            r = oracle_sample(c, args.ref_sample, nth)
+            out["cpu_baseline"] = {"value": 1.0 / r["t_full"], "unit": "evals/s", "cores": nth,
+                                   "kind": "oracle", "sample": r["sample"],
+                                   "sample_seconds": r["t_prep"] + r["t_llh"]}
+        print(json.dumps(out))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def roofline(dom, stats, c, fp64_peak, peaks, world, h8_ms, flops_total, h8_bytes_total):
+    """Roofline object for the dominant stage of the step."""
+    name, ms = dom
+    n, d, k = c["n"], c["d"], max(1, round(c["n"] / c["bs"]))
+    if "H8" in name:
+        ach = flops_total / world / (ms * 1e-3) / 1e12
+        return {"kernel": "k_h8 (fused per-block bordered Cholesky, DMMA)", "bound": "tensor",
+                "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak,
+                "traffic": None, "peak_source": "measured DMMA.8x8x4 FP64 (profiles/r01/fp64_peaks.jsonl)",
+                "algorithmic_per_launch": flops_total / world}
+    # kNN / RAC: FP64 ALU bound; algorithmic ops = 3 d FP64 flops per pair (sub, mul, add)
+    pairs = stats["knn_pairs"] if "H6" in name else (stats["rac_pairs"] / world if "H3" in name else None)
+    alu_peak = 148 * 64 * 2 * 1.965e9 / 1e12  # FP64 FMA lanes x 2 flops x max clock
+    if pairs is not None:
+        ach = pairs * 3 * d / (ms * 1e-3) / 1e12
+        return {"kernel": "k_knn" if "H6" in name else "k_rac", "bound": "alu", "achieved": ach,
+                "peak": alu_peak, "unit": "TFLOP/s", "frac": ach / alu_peak, "traffic": None,
+                "algorithmic_per_launch": pairs * 3 * d,
+                "peak_source": "148 SM x 64 FP64 lanes x 2 x 1965 MHz"}
+    hbm = peaks.get("hbm_gbs", 6550.0)
+    return {"kernel": name, "bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s",
+            "frac": None, "traffic": None}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--ref-sample", type=int, default=200_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
