@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <numeric>
+#include <unordered_map>
 
 #include "sbv_internal.cuh"
 
@@ -53,13 +54,19 @@ bool is_device_ptr(const void *p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
+// Capacity-tracked device buffers: re-prepare (e.g. an MLE rescale) reuses
+// allocations, so steady-state prepare never calls cudaMalloc/cudaFree
+// (both synchronise the device).
 template <class T>
-cudaError_t ensure(T *&p, size_t count, size_t &cap_bytes_unused) {
-  (void)cap_bytes_unused;
+cudaError_t ensure(T *&p, size_t count, std::unordered_map<void *, size_t> &cap) {
+  const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  auto it = cap.find((void *)&p);
+  if (p && it != cap.end() && it->second >= bytes) return cudaSuccess;
   if (p) cudaFree(p);
   p = nullptr;
-  if (count == 0) count = 1;
-  return cudaMalloc(&p, count * sizeof(T));
+  cudaError_t e = cudaMalloc(&p, bytes);
+  cap[(void *)&p] = e == cudaSuccess ? bytes : 0;
+  return e;
 }
 
 template <class T>
@@ -92,7 +99,9 @@ void free_state(sbv_ctx *h) {
   release(h->chunk_all);
   release(h->result);
   release(h->queue);
+  release(h->flag);
   release(h->ws);
+  h->cap.clear();
   h->prepared = false;
 }
 
@@ -262,9 +271,16 @@ int sbv_create(const sbv_opts *opts, sbv_handle *out) {
     h->profile = opts->profile;
   }
   for (int i = 0; i <= kMaxStages; i++) cudaEventCreate(&h->ev[i]);
-  if (cudaMallocHost(&h->result_host, 8 * sizeof(double)) != cudaSuccess) {
+  if (cudaMallocHost(&h->result_host, 8 * sizeof(double)) != cudaSuccess ||
+      cudaMallocHost(&h->flag_host, sizeof(int)) != cudaSuccess) {
     delete h;
     return SBV_ERR_OOM;
+  }
+  // keep stream-ordered temporaries (CUB sort scratch) pooled across calls
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, h->device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   *out = h;
   return SBV_OK;
@@ -279,6 +295,7 @@ void sbv_destroy(sbv_handle h) {
   for (int i = 0; i <= kMaxStages; i++)
     if (h->ev[i]) cudaEventDestroy(h->ev[i]);
   if (h->result_host) cudaFreeHost(h->result_host);
+  if (h->flag_host) cudaFreeHost(h->flag_host);
   delete h;
 }
 
@@ -321,7 +338,7 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   for (int j = 0; j < d; j++)
     if (!(scale[j] > 0) || !isfinite(scale[j])) return fail(h, SBV_ERR_ARG, "scale_j must be finite and > 0");
   CU(cudaSetDevice(h->device));
-  free_state(h);
+  h->prepared = false;
   h->n = n;
   h->d = d;
   h->bs = bs;
@@ -330,22 +347,16 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   const int64_t k = std::max<int64_t>(1, (2 * n + bs) / (2 * (int64_t)bs));  // round(n/bs)
   h->k = k;
   cudaStream_t st = h->stream;
-  size_t unused = 0;
+  auto &unused = h->cap;
   Timer tm(h, 1);
 
   CU(ensure(h->X, n * d, unused));
   CU(cudaMemcpyAsync(h->X, X, n * d * sizeof(double), cudaMemcpyDefault, st));
-  {
-    int *bad = nullptr;
-    CU(cudaMallocAsync(&bad, sizeof(int), st));
-    CU(cudaMemsetAsync(bad, 0, sizeof(int), st));
-    k_check_finite<<<grid_for(n * d), 256, 0, st>>>(h->X, n * d, bad);
-    int hb = 0;
-    CU(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    cudaFreeAsync(bad, st);
-    if (hb) return fail(h, SBV_ERR_ARG, "X has non-finite entries");
-  }
+  // finiteness flag: read back at the first host sync below (no extra stall)
+  CU(ensure(h->flag, 1, unused));
+  CU(cudaMemsetAsync(h->flag, 0, sizeof(int), st));
+  k_check_finite<<<grid_for(n * d), 256, 0, st>>>(h->X, n * d, h->flag);
+  CU(cudaMemcpyAsync(h->flag_host, h->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   tm.mark("h2d_X");
   CU(ensure(h->S, n * d, unused));
   CU(launch_scale(h->X, n, d, scale, h->S, st));
@@ -367,9 +378,6 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   tm.mark("H5_centroids");
 
   // shard: 64-block chunks of zeta order dealt round-robin over ranks
-  std::vector<int64_t> off_h(k + 1);
-  CU(cudaMemcpyAsync(off_h.data(), h->off, (k + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
   h->n_chunks = (k + kChunkBlocks - 1) / kChunkBlocks;
   std::vector<int32_t> local;
   local.reserve(k / h->world + kChunkBlocks);
@@ -391,8 +399,11 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
 
   // realised sizes -> LPT work order, statistics, H8 launch geometry
   std::vector<int32_t> cnt_h(h->k_local);
+  std::vector<int64_t> off_h(k + 1);
+  CU(cudaMemcpyAsync(off_h.data(), h->off, (k + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CU(cudaMemcpyAsync(cnt_h.data(), h->cnt, h->k_local * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
+  if (*h->flag_host) return fail(h, SBV_ERR_ARG, "X has non-finite entries");
   std::vector<int32_t> Nt(h->k_local);
   h->max_N = 0;
   h->min_bs = INT32_MAX;

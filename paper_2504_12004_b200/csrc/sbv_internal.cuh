@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/sbv.h"
@@ -57,11 +58,14 @@ struct Ctx {
   double *chunk_all = nullptr;    // world * n_chunks_local_pad x 4
   double *result = nullptr;       // 8 doubles: ell, quad, logdet, npts, nfail, fail_block, fail_stage, -
   double *result_host = nullptr;  // pinned 8 doubles
+  int *flag = nullptr;            // device: non-finite input flag
+  int *flag_host = nullptr;       // pinned mirror
   unsigned int *queue = nullptr;  // work counter
   double *ws = nullptr;           // H8 per-CTA L workspaces
   size_t ws_per_cta = 0;
   int h8_grid = 0;
   size_t h8_smem = 0;
+  std::unordered_map<void *, size_t> cap;  // device buffer capacities (bytes)
   // errors
   int64_t err_block = -1;
   int32_t err_stage = 0;
