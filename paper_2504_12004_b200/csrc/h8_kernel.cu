@@ -1,0 +1,659 @@
+// h8_kernel.cu — H8: the fused per-block log-likelihood kernel (Alg.5).
+//
+// For every block t this computes Alg.5 as ONE bordered Cholesky factorisation
+// of the joint covariance of [J_t; B_t] (m_t + bs_t points, N = m_t + bs_t):
+//
+//     [ Sigma_con     Sigma_cross ]  = L L^T,   L = [ L11   0  ]
+//     [ Sigma_cross^T Sigma_lk    ]                 [ L21  L22 ]
+//
+// L11 = POTRF(Sigma_con); L21^T = L11^{-1} Sigma_cross = Sigma'cross (TRSM);
+// L22 = POTRF(Sigma_lk - Sigma'cross^T Sigma'cross) = L' (GEMM + POTRF on
+// Sigma_new, Q1).  The observations ride along as one extra border
+// row [y_J^T y_B^T] whose forward solve is [y'_J ; v], v = L'^{-1}(y_B - mu)
+// (TRSV + GEMV + TRSV).  ell_t = -1/2 (sum_{j in B} v_j^2 + 2 sum_{j in B}
+// log L_jj) - bs_t/2 log 2pi (Q2).
+//
+// Schedule: one persistent CTA (8 warps) per block, 2 CTAs per SM, left-looking
+// over 32-column panels.  Per panel j, with the rows [32j, N] cut into chunks
+// of 32 rows handed out dynamically to warps:
+//   phase A  every chunk: Matérn covariance (Eq.5-6) generated straight into
+//            FP64 tensor-core accumulators (mma.sync m8n8k4 f64 = DMMA.8x8x4),
+//            minus L[rows, 0:32j] L[panel, 0:32j]^T, streamed from the
+//            L2-resident workspace; the result is parked in the panel's own
+//            workspace slot.  The diagonal chunk is handed out first and its
+//            warp factors the 32x32 diagonal tile (blocked by 8, DMMA inside)
+//            while the other warps are still updating the remaining chunks.
+//   phase B  every chunk: solve against the diagonal factor (blocked by 8,
+//            DMMA against the inverted 8x8 diagonal blocks), store L.
+// Workspace panels are stored as 8x4 fragment micro-tiles so every DMMA
+// operand fragment is one coalesced 256-byte warp load.
+//
+// Sign convention: accumulators hold -P (= L L^T - Sigma) so that the update
+// is a plain D = A B + C and no operand needs negation; the solve multiplies
+// by -inv(L_ss), which restores the sign of L.
+//
+// On B200 the FP64 tensor pipe and the FP64 ALU share one 64-FMA/clk/SM budget
+// (profiles/r01/fp64_peaks.jsonl), so covariance generation is trimmed:
+// coordinates are centred on the block and pre-multiplied by 1/beta once per
+// block (distance = d x (sub, fma)), and e^{-r} is a short Cody-Waite +
+// polynomial evaluation.
+#include <math.h>
+#include <stdlib.h>
+
+#include "sbv_internal.cuh"
+
+namespace sbv {
+
+constexpr int kH8Threads = 256;
+constexpr int kH8Warps = kH8Threads / 32;
+constexpr int kDld = kPanel + 1;  // diagonal tile leading dimension (bank skew)
+
+struct H8Args {
+  const double *Xp;      // n x d block-major ORIGINAL inputs
+  const double *yperm;   // n block-major observations
+  const int64_t *off;    // bc + 1
+  const int32_t *nbr;    // k_local x m positions (block-major), kNN order
+  const int32_t *cnt;    // k_local
+  const int32_t *local_blocks;
+  const int32_t *work_order;
+  int64_t k_local;
+  int m;  // nbr row stride
+  int d;
+  double sigma2, tau2;
+  double inv_beta[SBV_MAX_D];  // Eq.5: 1 / beta_j of theta
+  double *ws;                  // per-CTA L workspaces
+  size_t ws_per_cta;           // doubles
+  unsigned int *queue;
+  double *terms, *quads, *logdets;
+  int32_t *status;
+};
+
+__device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// e^{-r}, r >= 0: Cody-Waite reduction by ln 2 and a degree-12 Taylor
+// polynomial on |f| <= ln2/2 (about 2 ulp; 17 FP64 ops instead of ~23).
+__device__ __forceinline__ double exp_neg(double r) {
+  if (r > 708.0) return 0.0;
+  const double kL2E = 1.4426950408889634074;
+  const double kLn2Hi = 6.93147180369123816490e-01;
+  const double kLn2Lo = 1.90821492927058770002e-10;
+  const double k = rint(-r * kL2E);  // in [-1022, 0]
+  double f = fma(-k, kLn2Hi, -r);
+  f = fma(-k, kLn2Lo, f);
+  double p = 1.0 / 479001600.0;  // 1/12!
+  p = fma(p, f, 1.0 / 39916800.0);
+  p = fma(p, f, 1.0 / 3628800.0);
+  p = fma(p, f, 1.0 / 362880.0);
+  p = fma(p, f, 1.0 / 40320.0);
+  p = fma(p, f, 1.0 / 5040.0);
+  p = fma(p, f, 1.0 / 720.0);
+  p = fma(p, f, 1.0 / 120.0);
+  p = fma(p, f, 1.0 / 24.0);
+  p = fma(p, f, 1.0 / 6.0);
+  p = fma(p, f, 0.5);
+  p = fma(p, f, 1.0);
+  p = fma(p, f, 1.0);
+  const long long ki = (long long)k;
+  return p * __longlong_as_double((ki + 1023) << 52);
+}
+
+// Eq.6 in the paper's parameterisation (no sqrt(2 nu)), half-integer closed
+// forms (Q4), returned NEGATED (sign convention above).  NU2 = 2 nu.
+template <int NU2>
+__device__ __forceinline__ double neg_matern(double r, double msigma2) {
+  const double e = exp_neg(r) * msigma2;
+  if (NU2 == 1) return e;
+  if (NU2 == 3) return (1.0 + r) * e;
+  if (NU2 == 5) return fma(r, fma(r, 1.0 / 3.0, 1.0), 1.0) * e;
+  return fma(r, fma(r, fma(r, 1.0 / 15.0, 2.0 / 5.0), 1.0), 1.0) * e;
+}
+
+// Panel p of the workspace holds rows [32p, R) x 32 columns as row-blocks of
+// 8 rows; a row-block is 8 micro-tiles (4 columns each) x 32 doubles in lane
+// order (row = lane/4, column = lane%4).  Base of panel p, in doubles:
+__device__ __forceinline__ size_t panel_base(int p, int R) {
+  return (size_t)kPanel * ((size_t)p * R - (size_t)16 * p * (p - 1));
+}
+
+struct BlockCtx {
+  int c0, N, mt, Cp, R;
+  const double *vs;  // centred, 1/beta-scaled coordinates, N x d
+  const double *ys;  // border row values (y on real columns, 0 on padding)
+  int d;
+  double msigma2, mtau2;  // -sigma2, -tau2
+};
+
+// element offset of (local row lr, panel column c) in panel storage
+__device__ __forceinline__ int pan_off(int lr, int c) {
+  return (lr >> 3) * 256 + (c >> 2) * 32 + (lr & 7) * 4 + (c & 3);
+}
+
+// phase A (1): -covariance of the chunk rows [c0 + 8 tb, +8 nv) against the 32
+// panel columns, written into the chunk's panel slot.  Rolled loop, lane =
+// column (one copy of the Matérn code keeps the kernel inside the I-cache);
+// the upper triangle of the diagonal tile is skipped.
+template <int NU2>
+__device__ __forceinline__ void gen_chunk(double *pan, const BlockCtx &b, int tb, int nv, int lane) {
+  const int c = b.c0 + lane;
+  const double *xc = b.vs + (size_t)min(c, b.N - 1) * b.d;
+#pragma unroll 1
+  for (int rr = 0; rr < 8 * nv; rr++) {
+    const int lr = tb * 8 + rr, r = b.c0 + lr;
+    double v = 0.0;
+    if (r < b.N && c <= r && c < b.N) {
+      const double *xr = b.vs + (size_t)r * b.d;
+      double s = 0.0;
+      for (int jj = 0; jj < b.d; jj++) {  // Eq.5
+        const double u = xr[jj] - xc[jj];
+        s = fma(u, u, s);
+      }
+      v = neg_matern<NU2>(sqrt(s), b.msigma2);
+      if (r == c) v += b.mtau2;  // nugget on the diagonal only (Q3)
+    } else if (r == b.Cp) {
+      v = -b.ys[c];  // border row
+    } else if (r == c) {
+      v = -1.0;  // identity padding (r >= N)
+    }
+    pan[pan_off(lr, lane)] = v;
+  }
+}
+
+// phase A (2): acc += L[rows, 0:c0] L[c0:c0+32, 0:c0]^T on DMMA, operands from
+// the workspace (L2), 8 k-steps per previous panel, 2-stage prefetch.
+__device__ __forceinline__ void update_tiles(double (&acc)[4][4][2], const double *wsb, int c0,
+                                             int R, int tb, int nv, int lane) {
+  if (c0 == 0 || nv == 0) return;
+  const int np = c0 >> 5;
+  double ac[4], bc[4], an[4], bn[4];
+  const double *pp;
+  int offA[4], offB[4];
+  auto setp = [&](int p) {
+    pp = wsb + panel_base(p, R) + lane;
+#pragma unroll
+    for (int ct = 0; ct < 4; ct++) offB[ct] = (c0 + ct * 8 - p * kPanel) * 32;
+#pragma unroll
+    for (int rt = 0; rt < 4; rt++) offA[rt] = (c0 + (tb + min(rt, nv - 1)) * 8 - p * kPanel) * 32;
+  };
+  setp(0);
+#pragma unroll
+  for (int x = 0; x < 4; x++) {
+    bc[x] = pp[offB[x]];
+    ac[x] = pp[offA[x]];
+  }
+  for (int p = 0; p < np; p++) {
+#pragma unroll
+    for (int s = 0; s < 8; s++) {
+      if (s < 7) {
+#pragma unroll
+        for (int x = 0; x < 4; x++) {
+          bn[x] = pp[offB[x] + (s + 1) * 32];
+          an[x] = pp[offA[x] + (s + 1) * 32];
+        }
+      } else if (p + 1 < np) {
+        setp(p + 1);
+#pragma unroll
+        for (int x = 0; x < 4; x++) {
+          bn[x] = pp[offB[x]];
+          an[x] = pp[offA[x]];
+        }
+      }
+#pragma unroll
+      for (int rt = 0; rt < 4; rt++)
+        if (rt < nv)
+#pragma unroll
+          for (int ct = 0; ct < 4; ct++) dmma(acc[rt][ct][0], acc[rt][ct][1], ac[rt], bc[ct]);
+#pragma unroll
+      for (int x = 0; x < 4; x++) {
+        ac[x] = an[x];
+        bc[x] = bn[x];
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void park_tiles(const double (&acc)[4][4][2], double *pan, int tb, int nv,
+                                           int g, int q) {
+#pragma unroll
+  for (int rt = 0; rt < 4; rt++)
+    if (rt < nv)
+#pragma unroll
+      for (int ct = 0; ct < 4; ct++)
+        *reinterpret_cast<double2 *>(pan + pan_off((tb + rt) * 8 + g, ct * 8 + 2 * q)) =
+            make_double2(acc[rt][ct][0], acc[rt][ct][1]);
+}
+
+__device__ __forceinline__ void unpark_tiles(double (&acc)[4][4][2], const double *pan, int tb, int nv,
+                                             int g, int q) {
+#pragma unroll
+  for (int rt = 0; rt < 4; rt++)
+    if (rt < nv)
+#pragma unroll
+      for (int ct = 0; ct < 4; ct++) {
+        const double2 v = *reinterpret_cast<const double2 *>(pan + pan_off((tb + rt) * 8 + g, ct * 8 + 2 * q));
+        acc[rt][ct][0] = v.x;
+        acc[rt][ct][1] = v.y;
+      }
+}
+
+// C-layout 8x8 accumulator pair -> A fragment of k-step kk (two shuffles)
+__device__ __forceinline__ double c_to_a(const double (&t)[2], int g, int q, int kk) {
+  const int src = (g << 2) | (2 * kk + (q >> 1));
+  const double v0 = __shfl_sync(0xffffffffu, t[0], src);
+  const double v1 = __shfl_sync(0xffffffffu, t[1], src);
+  return (q & 1) ? v1 : v0;
+}
+
+// phase B: rows below the diagonal tile: L_rows = P_rows L_jj^{-T}, blocked over
+// the four 8-column sub-blocks s (all products on DMMA), acc holding -P:
+//   T'_s = -P_s + sum_{u<s} X_u L_su^T = -T_s ;   X_s = T'_s (-inv(L_ss))^T
+// Dt holds L_jj, Mn holds -inv(L_ss) on the diagonal 8x8 blocks.
+__device__ __forceinline__ void trsm_tiles(double (&acc)[4][4][2], const double *Dt, const double *Mn,
+                                           int nv, int g, int q) {
+#pragma unroll
+  for (int rt = 0; rt < 4; rt++) {
+    if (rt < nv) {
+      double xa[3][2];  // finished X_u in A layout (k-steps kk = 0, 1)
+#pragma unroll
+      for (int s = 0; s < 4; s++) {
+        double t[2] = {acc[rt][s][0], acc[rt][s][1]};
+#pragma unroll
+        for (int u = 0; u < s; u++)
+#pragma unroll
+          for (int kk = 0; kk < 2; kk++)
+            dmma(t[0], t[1], xa[u][kk], Dt[(8 * s + g) * kDld + 8 * u + 4 * kk + q]);
+        double x[2] = {0.0, 0.0};
+#pragma unroll
+        for (int kk = 0; kk < 2; kk++)
+          dmma(x[0], x[1], c_to_a(t, g, q, kk), Mn[(8 * s + g) * kDld + 8 * s + 4 * kk + q]);
+        acc[rt][s][0] = x[0];
+        acc[rt][s][1] = x[1];
+        if (s < 3) {
+#pragma unroll
+          for (int kk = 0; kk < 2; kk++) xa[s][kk] = c_to_a(x, g, q, kk);
+        }
+      }
+    }
+  }
+}
+
+// The panel's 32x32 diagonal tile, by one warp, blocked by 8: for each
+// 8-column sub-block s: factor the 8x8 diagonal block in registers (lane i
+// owns row i, column entries broadcast by shuffles), invert it (lane j owns
+// column j), solve the rows below with DMMA against the inverse and apply the
+// trailing SYRK update with DMMA, all in shared memory.
+// Dt: in = tile (+P), out = L_jj (+ 1/L_ii in column 32);
+// Mn: out = -inv(L_ss) on the four diagonal 8x8 blocks (zero above).
+__device__ __forceinline__ void diag_factor(double *Dt, double *Mn, int lane, const BlockCtx &b,
+                                            double &logdet_acc, int &s_fail, int &s_fail_stage) {
+  const int g = lane >> 2, q = lane & 3;
+  const int r8 = lane & 7;
+#pragma unroll 1
+  for (int s = 0; s < 4; s++) {
+    const int o = 8 * s;
+    double a[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) a[j] = Dt[(o + r8) * kDld + o + j];
+    double rd_own = 1.0, l_own = 1.0;
+    int bad_k = 8;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      double piv = __shfl_sync(0xffffffffu, a[k], k);
+      if (!(piv > 0.0) || !isfinite(piv)) {
+        bad_k = min(bad_k, k);
+        piv = 1.0;
+      }
+      const double r = rsqrt(piv);
+      const double lkk = piv * r;
+      if (r8 == k) {
+        a[k] = lkk;
+        l_own = lkk;
+        rd_own = r;
+      } else if (r8 > k) {
+        a[k] *= r;
+      }
+#pragma unroll
+      for (int j = k + 1; j < 8; j++) {
+        const double ljk = __shfl_sync(0xffffffffu, a[k], j);
+        if (r8 >= j) a[j] = fma(-a[k], ljk, a[j]);
+      }
+    }
+    if (bad_k < 8 && lane == 0 && s_fail == 0) {
+      s_fail = 1;
+      s_fail_stage = (b.c0 + o + bad_k < b.mt) ? 1 : 2;
+    }
+    if (lane < 8) {
+      const int col = b.c0 + o + lane;
+      if (col >= b.mt && col < b.N) logdet_acc += log(l_own);
+#pragma unroll
+      for (int j = 0; j < 8; j++) Dt[(o + lane) * kDld + o + j] = j <= lane ? a[j] : 0.0;
+      Dt[(o + lane) * kDld + kPanel] = rd_own;
+    }
+    __syncwarp();
+    if (lane < 8) {  // -inv(L_ss): lane j owns column j
+      double x[8];
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < i; k++) acc = fma(Dt[(o + i) * kDld + o + k], x[k], acc);
+        const double ri = Dt[(o + i) * kDld + kPanel];
+        x[i] = lane == i ? ri : (lane < i ? -acc * ri : 0.0);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; i++) Mn[(o + i) * kDld + o + lane] = -x[i];
+    }
+    __syncwarp();
+    if (s == 3) break;
+    // rows below: L_ts = D_ts inv(L_ss)^T = (-D_ts) (-inv(L_ss))^T
+    for (int t = s + 1; t < 4; t++) {
+      const int ot = 8 * t;
+      double c[2] = {0.0, 0.0};
+#pragma unroll
+      for (int kk = 0; kk < 2; kk++)
+        dmma(c[0], c[1], -Dt[(ot + g) * kDld + o + 4 * kk + q], Mn[(o + g) * kDld + o + 4 * kk + q]);
+      __syncwarp();
+      Dt[(ot + g) * kDld + o + 2 * q] = c[0];
+      Dt[(ot + g) * kDld + o + 2 * q + 1] = c[1];
+      __syncwarp();
+    }
+    // trailing update D_tu -= L_ts L_us^T for s < u <= t
+    for (int t = s + 1; t < 4; t++) {
+      for (int u = s + 1; u <= t; u++) {
+        const int ot = 8 * t, ou = 8 * u;
+        double c[2] = {Dt[(ot + g) * kDld + ou + 2 * q], Dt[(ot + g) * kDld + ou + 2 * q + 1]};
+#pragma unroll
+        for (int kk = 0; kk < 2; kk++)
+          dmma(c[0], c[1], -Dt[(ot + g) * kDld + o + 4 * kk + q], Dt[(ou + g) * kDld + o + 4 * kk + q]);
+        __syncwarp();
+        Dt[(ot + g) * kDld + ou + 2 * q] = c[0];
+        Dt[(ot + g) * kDld + ou + 2 * q + 1] = c[1];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+__device__ __forceinline__ int next_chunk(int *counter, int lane) {
+  int ch = 0;
+  if (lane == 0) ch = atomicAdd(counter, 1);
+  return __shfl_sync(0xffffffffu, ch, 0);
+}
+
+template <int NU2, int MINB>
+__global__ void __launch_bounds__(kH8Threads, MINB) k_h8(H8Args a) {
+  extern __shared__ double smem[];
+  __shared__ int s_item, s_fail, s_fail_stage, s_chunkA, s_chunkB, s_pregen, s_gen_next, s_factored;
+  __shared__ double s_red[2 * kH8Warps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int d = a.d;
+  double *wsb = a.ws + (size_t)blockIdx.x * a.ws_per_cta;
+  double *Dt = smem;               // 32 x kDld: diagonal tile, then L_jj
+  double *Mn = Dt + kPanel * kDld; // 32 x kDld: -inv(L_ss) blocks
+  double *ib = Mn + kPanel * kDld; // SBV_MAX_D inverse ranges
+  double *xref = ib + SBV_MAX_D;   // SBV_MAX_D block reference point
+  double *ys = xref + SBV_MAX_D;   // Cp_max + 8 border values
+  for (int j = tid; j < d; j += kH8Threads) ib[j] = a.inv_beta[j];
+
+  for (;;) {
+    if (tid == 0) s_item = (int)atomicAdd(a.queue, 1u);
+    __syncthreads();
+    const int item = s_item;
+    if (item >= a.k_local) break;
+    const int li = a.work_order[item];
+    const int64_t t = a.local_blocks[li];
+    BlockCtx b;
+    b.mt = a.cnt[li];
+    const int64_t b0 = a.off[t];
+    const int bst = (int)(a.off[t + 1] - b0);
+    b.N = b.mt + bst;
+    b.Cp = (b.N + kPanel - 1) / kPanel * kPanel;
+    b.R = b.Cp + 8;  // rows: matrix (Cp) + border row + 7 zero rows
+    b.d = d;
+    b.msigma2 = -a.sigma2;
+    b.mtau2 = -a.tau2;
+    b.ys = ys;
+    double *vs = ys + b.Cp + 8;
+    b.vs = vs;
+    const int NP = b.Cp / kPanel;
+
+    // stage [J_t; B_t]: coordinates centred on the block's first member and
+    // scaled by 1/beta (Eq.5), observations of the border row
+    for (int j = tid; j < d; j += kH8Threads) xref[j] = a.Xp[b0 * d + j];
+    __syncthreads();
+    for (int e = tid; e < b.N * d; e += kH8Threads) {
+      const int i = e / d, j = e - i * d;
+      const int64_t pos = i < b.mt ? (int64_t)a.nbr[(int64_t)li * a.m + i] : b0 + (i - b.mt);
+      vs[e] = (a.Xp[pos * d + j] - xref[j]) * ib[j];
+    }
+    for (int i = tid; i < b.Cp + 8; i += kH8Threads) {
+      double v = 0.0;
+      if (i < b.N) {
+        const int64_t pos = i < b.mt ? (int64_t)a.nbr[(int64_t)li * a.m + i] : b0 + (i - b.mt);
+        v = a.yperm[pos];
+      }
+      ys[i] = v;
+    }
+    if (tid == 0) {
+      s_fail = 0;
+      s_fail_stage = 0;
+      s_chunkA = 0;
+      s_chunkB = 0;
+      s_pregen = 0;
+      s_gen_next = 0;
+      s_factored = 0;
+    }
+    __syncthreads();
+
+    double quad_acc = 0.0, logdet_acc = 0.0;
+    for (int j = 0; j < NP; j++) {
+      b.c0 = j * kPanel;
+      const int nrt = (b.R - b.c0) >> 3;  // row tiles in this panel
+      const int nch = (nrt + 3) >> 2;     // chunks of 4 row tiles; chunk 0 = diagonal tile
+      double *pan = wsb + panel_base(j, b.R);
+      double acc[4][4][2];
+      const int pre = min(s_pregen, nch);  // chunks generated ahead during panel j-1
+      // ---- phase A: generate + update every chunk; park -P in the panel slot
+      for (int ch = next_chunk(&s_chunkA, lane); ch < nch; ch = next_chunk(&s_chunkA, lane)) {
+        const int tb = 4 * ch, nv = min(4, nrt - tb);
+        if (ch >= pre) {
+          gen_chunk<NU2>(pan, b, tb, nv, lane);
+          __syncwarp();
+        }
+        unpark_tiles(acc, pan, tb, nv, g, q);
+        update_tiles(acc, wsb, b.c0, b.R, tb, nv, lane);
+        if (ch == 0) {  // the diagonal tile: factor it right away
+#pragma unroll
+          for (int rt = 0; rt < 4; rt++)
+#pragma unroll
+            for (int ct = 0; ct < 4; ct++)
+#pragma unroll
+              for (int i = 0; i < 2; i++) Dt[(rt * 8 + g) * kDld + ct * 8 + 2 * q + i] = -acc[rt][ct][i];
+          __syncwarp();
+          diag_factor(Dt, Mn, lane, b, logdet_acc, s_fail, s_fail_stage);
+          __syncwarp();
+          if (lane == 0) *(volatile int *)&s_factored = 1;
+        } else {
+          park_tiles(acc, pan, tb, nv, g, q);
+        }
+      }
+      // ---- while the diagonal tile is being factored: generate panel j+1's
+      //      covariance ahead (it depends on nothing), one chunk per task
+      if (j + 1 < NP) {
+        BlockCtx bn = b;
+        bn.c0 = b.c0 + kPanel;
+        const int nrt_n = (b.R - bn.c0) >> 3, nch_n = (nrt_n + 3) >> 2;
+        double *pan_n = wsb + panel_base(j + 1, b.R);
+        while (*(volatile int *)&s_factored == 0) {
+          const int gc = next_chunk(&s_gen_next, lane);
+          if (gc >= nch_n) break;
+          gen_chunk<NU2>(pan_n, bn, 4 * gc, min(4, nrt_n - 4 * gc), lane);
+        }
+      }
+      __syncthreads();  // diagonal factor ready, all chunks parked
+      if (tid == 0) {
+        s_chunkA = 0;
+        s_pregen = s_gen_next;  // every handed-out pre-generation task is complete here
+        s_gen_next = 0;
+        s_factored = 0;
+      }
+      // ---- phase B: solve and store every chunk
+      const int rb = (b.Cp - b.c0) >> 3;  // row tile of the border row
+      for (int ch = next_chunk(&s_chunkB, lane); ch < nch; ch = next_chunk(&s_chunkB, lane)) {
+        const int tb = 4 * ch, nv = min(4, nrt - tb);
+        if (ch == 0) {
+#pragma unroll
+          for (int rt = 0; rt < 4; rt++)
+#pragma unroll
+            for (int ct = 0; ct < 4; ct++)
+#pragma unroll
+              for (int i = 0; i < 2; i++) {
+                const int rr = rt * 8 + g, cc = ct * 8 + 2 * q + i;
+                acc[rt][ct][i] = cc <= rr ? Dt[rr * kDld + cc] : 0.0;
+              }
+        } else {
+          unpark_tiles(acc, pan, tb, nv, g, q);
+          trsm_tiles(acc, Dt, Mn, nv, g, q);
+        }
+        park_tiles(acc, pan, tb, nv, g, q);
+        if (rb >= tb && rb < tb + nv && g == 0) {  // border row: v^T v
+#pragma unroll
+          for (int rt = 0; rt < 4; rt++)
+            if (tb + rt == rb)
+#pragma unroll
+              for (int ct = 0; ct < 4; ct++)
+#pragma unroll
+                for (int i = 0; i < 2; i++) {
+                  const int col = b.c0 + ct * 8 + 2 * q + i;
+                  if (col >= b.mt && col < b.N) quad_acc = fma(acc[rt][ct][i], acc[rt][ct][i], quad_acc);
+                }
+        }
+      }
+      __syncthreads();  // panel j complete and visible before panel j+1 reads it
+      if (tid == 0) s_chunkB = 0;
+      if (s_fail) break;
+    }
+
+    // ---- block reduction of quad / logdet (fixed order)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      quad_acc += __shfl_xor_sync(0xffffffffu, quad_acc, o);
+      logdet_acc += __shfl_xor_sync(0xffffffffu, logdet_acc, o);
+    }
+    if (lane == 0) {
+      s_red[warp] = quad_acc;
+      s_red[kH8Warps + warp] = logdet_acc;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double qs = 0.0, ls = 0.0;
+      for (int w = 0; w < kH8Warps; w++) {
+        qs += s_red[w];
+        ls += s_red[kH8Warps + w];
+      }
+      ls *= 2.0;
+      const double term = -0.5 * (qs + ls) - 0.5 * (double)bst * 1.8378770664093454836;  // log 2pi
+      a.terms[li] = s_fail ? NAN : term;
+      a.quads[li] = qs;
+      a.logdets[li] = ls;
+      a.status[li] = s_fail ? s_fail_stage : 0;
+    }
+    __syncthreads();
+  }
+}
+
+size_t h8_smem_bytes(int max_N, int d) {
+  const size_t Cp = (max_N + kPanel - 1) / kPanel * kPanel;
+  return sizeof(double) * (2 * (size_t)kPanel * kDld + 2 * SBV_MAX_D + (Cp + 8) + (size_t)max_N * d);
+}
+
+size_t h8_ws_doubles(int max_N) {
+  const size_t Cp = (max_N + kPanel - 1) / kPanel * kPanel, R = Cp + 8, NP = Cp / kPanel;
+  size_t tot = 0;
+  for (size_t p = 0; p < NP; p++) tot += kPanel * (R - kPanel * p);
+  return (tot + 63) / 64 * 64;
+}
+
+template <int NU2, int MINB>
+static cudaError_t set_attr(size_t smem) {
+  return cudaFuncSetAttribute(k_h8<NU2, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+// CTAs per SM the H8 kernel is compiled for (SBV_H8_MINB=1 selects the
+// 1-CTA/SM register-rich variant; default 2).
+static int h8_minb() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("SBV_H8_MINB");
+    v = (e && atoi(e) == 1) ? 1 : 2;
+  }
+  return v;
+}
+
+int h8_max_ctas_per_sm(size_t smem) {
+  int nb = 0;
+  if (h8_minb() == 1) {
+    set_attr<5, 1>(smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_h8<5, 1>, kH8Threads, smem);
+  } else {
+    set_attr<5, 2>(smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_h8<5, 2>, kH8Threads, smem);
+  }
+  return nb;
+}
+
+template <int NU2>
+static void launch_nu(int grid, size_t smem, cudaStream_t st, const H8Args &a) {
+  if (h8_minb() == 1) {
+    set_attr<NU2, 1>(smem);
+    k_h8<NU2, 1><<<grid, kH8Threads, smem, st>>>(a);
+  } else {
+    set_attr<NU2, 2>(smem);
+    k_h8<NU2, 2><<<grid, kH8Threads, smem, st>>>(a);
+  }
+}
+
+cudaError_t launch_h8(const Ctx &c, const double *theta, cudaStream_t st) {
+  H8Args a;
+  a.Xp = c.Xperm;
+  a.yperm = c.yperm;
+  a.off = c.off;
+  a.nbr = c.nbr;
+  a.cnt = c.cnt;
+  a.local_blocks = c.local_blocks;
+  a.work_order = c.work_order;
+  a.k_local = c.k_local;
+  a.m = c.m > 0 ? c.m : 1;
+  a.d = c.d;
+  a.sigma2 = theta[0];
+  a.tau2 = theta[c.d + 2];
+  for (int j = 0; j < SBV_MAX_D; j++) a.inv_beta[j] = j < c.d ? 1.0 / theta[1 + j] : 0.0;
+  a.ws = c.ws;
+  a.ws_per_cta = c.ws_per_cta;
+  a.queue = c.queue;
+  a.terms = c.terms;
+  a.quads = c.quads;
+  a.logdets = c.logdets;
+  a.status = c.status;
+  const double nu = theta[c.d + 1];
+  cudaError_t e = cudaMemsetAsync(c.queue, 0, sizeof(unsigned int), st);
+  if (e) return e;
+  if (c.k_local == 0) return cudaSuccess;
+  const int grid = c.h8_grid;
+  const size_t smem = c.h8_smem;
+  if (nu == 0.5)
+    launch_nu<1>(grid, smem, st, a);
+  else if (nu == 1.5)
+    launch_nu<3>(grid, smem, st, a);
+  else if (nu == 2.5)
+    launch_nu<5>(grid, smem, st, a);
+  else
+    launch_nu<7>(grid, smem, st, a);
+  return cudaGetLastError();
+}
+
+}  // namespace sbv
