@@ -66,6 +66,8 @@ struct H8Args {
   unsigned int *queue;
   double *terms, *quads, *logdets;
   int32_t *status;
+  int np_max;     // panels of the largest block
+  int max_tasks;  // task-list capacity
 };
 
 __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
@@ -164,48 +166,44 @@ __device__ __forceinline__ void gen_chunk(double *pan, const BlockCtx &b, int tb
 
 // phase A (2): acc += L[rows, 0:c0] L[c0:c0+32, 0:c0]^T on DMMA, operands from
 // the workspace (L2), 8 k-steps per previous panel, 2-stage prefetch.
+// Only previous panels [p0, p1) are applied (update-ahead splits the range).
 __device__ __forceinline__ void update_tiles(double (&acc)[4][4][2], const double *wsb, int c0,
-                                             int R, int tb, int nv, int lane) {
-  if (c0 == 0 || nv == 0) return;
-  const int np = c0 >> 5;
-  double ac[4], bc[4], an[4], bn[4];
-  const double *pp;
-  int offA[4], offB[4];
+                                             int R, int tb, int nv, int lane, int p0, int p1) {
+  if (p1 <= p0 || nv == 0) return;
+  // Row tiles past nv (a chunk's ragged tail) read the last valid row tile and
+  // their results are never stored: the DMMA stream stays unpredicated.
+  const int rowA = c0 + 8 * tb;
+  const int dA1 = 256 * min(1, nv - 1), dA2 = 256 * min(2, nv - 1), dA3 = 256 * min(3, nv - 1);
+  const double *Ab, *Bb;  // this panel's chunk rows / diagonal rows (+ lane)
   auto setp = [&](int p) {
-    pp = wsb + panel_base(p, R) + lane;
-#pragma unroll
-    for (int ct = 0; ct < 4; ct++) offB[ct] = (c0 + ct * 8 - p * kPanel) * 32;
-#pragma unroll
-    for (int rt = 0; rt < 4; rt++) offA[rt] = (c0 + (tb + min(rt, nv - 1)) * 8 - p * kPanel) * 32;
+    const double *base = wsb + panel_base(p, R) + lane;
+    Ab = base + (size_t)(rowA - p * kPanel) * 32;
+    Bb = base + (size_t)(c0 - p * kPanel) * 32;
   };
-  setp(0);
+  double ac[4], bc[4], an[4], bn[4];
+  auto load = [&](int s, double (&A)[4], double (&B)[4]) {
 #pragma unroll
-  for (int x = 0; x < 4; x++) {
-    bc[x] = pp[offB[x]];
-    ac[x] = pp[offA[x]];
-  }
-  for (int p = 0; p < np; p++) {
+    for (int ct = 0; ct < 4; ct++) B[ct] = Bb[ct * 256 + s * 32];
+    A[0] = Ab[s * 32];
+    A[1] = Ab[dA1 + s * 32];
+    A[2] = Ab[dA2 + s * 32];
+    A[3] = Ab[dA3 + s * 32];
+  };
+  setp(p0);
+  load(0, ac, bc);
+  for (int p = p0; p < p1; p++) {
 #pragma unroll
     for (int s = 0; s < 8; s++) {
       if (s < 7) {
-#pragma unroll
-        for (int x = 0; x < 4; x++) {
-          bn[x] = pp[offB[x] + (s + 1) * 32];
-          an[x] = pp[offA[x] + (s + 1) * 32];
-        }
-      } else if (p + 1 < np) {
+        load(s + 1, an, bn);
+      } else if (p + 1 < p1) {
         setp(p + 1);
-#pragma unroll
-        for (int x = 0; x < 4; x++) {
-          bn[x] = pp[offB[x]];
-          an[x] = pp[offA[x]];
-        }
+        load(0, an, bn);
       }
 #pragma unroll
       for (int rt = 0; rt < 4; rt++)
-        if (rt < nv)
 #pragma unroll
-          for (int ct = 0; ct < 4; ct++) dmma(acc[rt][ct][0], acc[rt][ct][1], ac[rt], bc[ct]);
+        for (int ct = 0; ct < 4; ct++) dmma(acc[rt][ct][0], acc[rt][ct][1], ac[rt], bc[ct]);
 #pragma unroll
       for (int x = 0; x < 4; x++) {
         ac[x] = an[x];
@@ -377,26 +375,53 @@ __device__ __forceinline__ void diag_factor(double *Dt, double *Mn, int lane, co
   }
 }
 
-__device__ __forceinline__ int next_chunk(int *counter, int lane) {
-  int ch = 0;
-  if (lane == 0) ch = atomicAdd(counter, 1);
-  return __shfl_sync(0xffffffffu, ch, 0);
+// ---------------------------------------------------------------------------
+// Per-block task graph (no CTA-wide barriers inside a block).  Panel j has
+// nch_j = nch_{j-1} - 1 chunks of 32 rows (chunk ch of panel j covers the rows
+// of chunk ch+1 of panel j-1).  Tasks:
+//   A(j,ch)  generate -Sigma for the chunk and apply panels [0, j-1)      -> parked
+//   F(j)     chunk 0: apply panel j-1, factor the diagonal tile (Dt/Mn[j%2])
+//   C0(j)    store L_jj
+//   BC(j,ch) ch >= 1: apply panel j-1, solve against L_jj, store L
+// Dependencies (all earlier in the dispensing order below, so in-order
+// dispensing with spin-waits cannot deadlock):
+//   A(j,ch)  : every chunk of panels <= j-2 stored
+//   F(j)     : A(j,0); chunk 1 of panel j-1 stored; every chunk of panel j-2
+//              stored (Dt/Mn buffer reuse)
+//   C0(j)    : F(j)
+//   BC(j,ch) : A(j,ch); chunks 1 and ch+1 of panel j-1 stored; F(j)
+// Order: A(0,*) A(1,*) F(0) C0(0) BC(0,1) F(1) BC(0,2..) A(2,*) C0(1) BC(1,1)
+//        F(2) BC(1,2..) A(3,*) ...   -- F(j+1) runs right after chunk 1 of
+// panel j is stored (look-ahead), while the other warps solve the rest of
+// panel j and start panel j+2.
+enum : int { kTaskA = 0, kTaskF = 1, kTaskC0 = 2, kTaskBC = 3 };
+
+__device__ __forceinline__ int enc_task(int type, int j, int ch) { return (type << 24) | (j << 12) | ch; }
+
+__device__ __forceinline__ void spin_until(const volatile int *p, int target) {
+  while (*p < target) __nanosleep(32);
 }
 
 template <int NU2, int MINB>
 __global__ void __launch_bounds__(kH8Threads, MINB) k_h8(H8Args a) {
   extern __shared__ double smem[];
-  __shared__ int s_item, s_fail, s_fail_stage, s_chunkA, s_chunkB, s_pregen, s_gen_next, s_factored;
+  __shared__ int s_item, s_fail, s_fail_stage, s_task, s_ntask;
   __shared__ double s_red[2 * kH8Warps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int d = a.d;
+  const int npmax = a.np_max, nchmax = npmax + 1;
   double *wsb = a.ws + (size_t)blockIdx.x * a.ws_per_cta;
-  double *Dt = smem;               // 32 x kDld: diagonal tile, then L_jj
-  double *Mn = Dt + kPanel * kDld; // 32 x kDld: -inv(L_ss) blocks
-  double *ib = Mn + kPanel * kDld; // SBV_MAX_D inverse ranges
-  double *xref = ib + SBV_MAX_D;   // SBV_MAX_D block reference point
-  double *ys = xref + SBV_MAX_D;   // Cp_max + 8 border values
+  double *Dt2 = smem;                  // 2 x 32 x kDld: diagonal tile / L_jj (by panel parity)
+  double *Mn2 = Dt2 + 2 * kPanel * kDld; // 2 x 32 x kDld: -inv(L_ss) blocks
+  double *ib = Mn2 + 2 * kPanel * kDld;  // SBV_MAX_D inverse ranges
+  double *xref = ib + SBV_MAX_D;         // SBV_MAX_D block reference point
+  int *doneA = reinterpret_cast<int *>(xref + SBV_MAX_D);  // [npmax][nchmax]
+  int *doneC = doneA + npmax * nchmax;                     // [npmax][nchmax] chunk stored
+  int *cntC = doneC + npmax * nchmax;                      // [npmax] chunks stored
+  int *doneF = cntC + npmax;                               // [npmax]
+  int *tasks = doneF + npmax;                              // task list
+  double *ys = reinterpret_cast<double *>(tasks + ((a.max_tasks + 1) & ~1));  // Cp_max + 8
   for (int j = tid; j < d; j += kH8Threads) ib[j] = a.inv_beta[j];
 
   for (;;) {
@@ -420,10 +445,12 @@ __global__ void __launch_bounds__(kH8Threads, MINB) k_h8(H8Args a) {
     double *vs = ys + b.Cp + 8;
     b.vs = vs;
     const int NP = b.Cp / kPanel;
+    const int nch0 = ((b.R >> 3) + 3) >> 2;  // chunks of panel 0; panel j has nch0 - j
 
     // stage [J_t; B_t]: coordinates centred on the block's first member and
-    // scaled by 1/beta (Eq.5), observations of the border row
+    // scaled by 1/beta (Eq.5), observations of the border row; reset flags
     for (int j = tid; j < d; j += kH8Threads) xref[j] = a.Xp[b0 * d + j];
+    for (int i = tid; i < 2 * npmax * nchmax + 2 * npmax; i += kH8Threads) doneA[i] = 0;
     __syncthreads();
     for (int e = tid; e < b.N * d; e += kH8Threads) {
       const int i = e / d, j = e - i * d;
@@ -438,74 +465,90 @@ __global__ void __launch_bounds__(kH8Threads, MINB) k_h8(H8Args a) {
       }
       ys[i] = v;
     }
-    if (tid == 0) {
+    if (tid == 0) {  // dispensing order (see above)
+      int n = 0;
+      auto addA = [&](int j) {
+        if (j < NP)
+          for (int ch = 0; ch < nch0 - j; ch++) tasks[n++] = enc_task(kTaskA, j, ch);
+      };
+      addA(0);
+      addA(1);
+      tasks[n++] = enc_task(kTaskF, 0, 0);
+      for (int j = 0; j < NP; j++) {
+        const int nch = nch0 - j;
+        tasks[n++] = enc_task(kTaskC0, j, 0);
+        tasks[n++] = enc_task(kTaskBC, j, 1);
+        if (j + 1 < NP) tasks[n++] = enc_task(kTaskF, j + 1, 0);
+        for (int ch = 2; ch < nch; ch++) tasks[n++] = enc_task(kTaskBC, j, ch);
+        addA(j + 2);
+      }
+      s_ntask = n;
+      s_task = 0;
       s_fail = 0;
       s_fail_stage = 0;
-      s_chunkA = 0;
-      s_chunkB = 0;
-      s_pregen = 0;
-      s_gen_next = 0;
-      s_factored = 0;
     }
     __syncthreads();
 
     double quad_acc = 0.0, logdet_acc = 0.0;
-    for (int j = 0; j < NP; j++) {
-      b.c0 = j * kPanel;
-      const int nrt = (b.R - b.c0) >> 3;  // row tiles in this panel
-      const int nch = (nrt + 3) >> 2;     // chunks of 4 row tiles; chunk 0 = diagonal tile
+    const int ntask = s_ntask;
+    const int rb_abs = b.Cp;  // border row index
+    for (;;) {
+      int ti = 0;
+      if (lane == 0) ti = atomicAdd(&s_task, 1);
+      ti = __shfl_sync(0xffffffffu, ti, 0);
+      if (ti >= ntask) break;
+      const int code = tasks[ti];
+      const int type = code >> 24, j = (code >> 12) & 0xfff, ch = code & 0xfff;
+      const int c0 = j * kPanel;
+      b.c0 = c0;
+      const int nrt = (b.R - c0) >> 3;
+      const int tb = 4 * ch, nv = min(4, nrt - tb);
       double *pan = wsb + panel_base(j, b.R);
+      double *Dt = Dt2 + (j & 1) * kPanel * kDld;
+      double *Mn = Mn2 + (j & 1) * kPanel * kDld;
       double acc[4][4][2];
-      const int pre = min(s_pregen, nch);  // chunks generated ahead during panel j-1
-      // ---- phase A: generate + update every chunk; park -P in the panel slot
-      for (int ch = next_chunk(&s_chunkA, lane); ch < nch; ch = next_chunk(&s_chunkA, lane)) {
-        const int tb = 4 * ch, nv = min(4, nrt - tb);
-        if (ch >= pre) {
-          gen_chunk<NU2>(pan, b, tb, nv, lane);
+      if (type == kTaskA) {
+        if (j >= 2) spin_until(&cntC[j - 2], nch0 - (j - 2));
+        __threadfence_block();
+        gen_chunk<NU2>(pan, b, tb, nv, lane);
+        if (j >= 2) {
           __syncwarp();
-        }
-        unpark_tiles(acc, pan, tb, nv, g, q);
-        update_tiles(acc, wsb, b.c0, b.R, tb, nv, lane);
-        if (ch == 0) {  // the diagonal tile: factor it right away
-#pragma unroll
-          for (int rt = 0; rt < 4; rt++)
-#pragma unroll
-            for (int ct = 0; ct < 4; ct++)
-#pragma unroll
-              for (int i = 0; i < 2; i++) Dt[(rt * 8 + g) * kDld + ct * 8 + 2 * q + i] = -acc[rt][ct][i];
-          __syncwarp();
-          diag_factor(Dt, Mn, lane, b, logdet_acc, s_fail, s_fail_stage);
-          __syncwarp();
-          if (lane == 0) *(volatile int *)&s_factored = 1;
-        } else {
+          unpark_tiles(acc, pan, tb, nv, g, q);
+          update_tiles(acc, wsb, c0, b.R, tb, nv, lane, 0, j - 1);
           park_tiles(acc, pan, tb, nv, g, q);
         }
-      }
-      // ---- while the diagonal tile is being factored: generate panel j+1's
-      //      covariance ahead (it depends on nothing), one chunk per task
-      if (j + 1 < NP) {
-        BlockCtx bn = b;
-        bn.c0 = b.c0 + kPanel;
-        const int nrt_n = (b.R - bn.c0) >> 3, nch_n = (nrt_n + 3) >> 2;
-        double *pan_n = wsb + panel_base(j + 1, b.R);
-        while (*(volatile int *)&s_factored == 0) {
-          const int gc = next_chunk(&s_gen_next, lane);
-          if (gc >= nch_n) break;
-          gen_chunk<NU2>(pan_n, bn, 4 * gc, min(4, nrt_n - 4 * gc), lane);
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0) *(volatile int *)&doneA[j * nchmax + ch] = 1;
+      } else if (type == kTaskF) {
+        spin_until(&doneA[j * nchmax], 1);
+        if (j >= 1) spin_until(&doneC[(j - 1) * nchmax + 1], 1);
+        if (j >= 2) spin_until(&cntC[j - 2], nch0 - (j - 2));
+        __threadfence_block();
+        unpark_tiles(acc, pan, 0, 4, g, q);
+        if (j >= 1) update_tiles(acc, wsb, c0, b.R, 0, 4, lane, j - 1, j);
+#pragma unroll
+        for (int rt = 0; rt < 4; rt++)
+#pragma unroll
+          for (int ct = 0; ct < 4; ct++)
+#pragma unroll
+            for (int i = 0; i < 2; i++) Dt[(rt * 8 + g) * kDld + ct * 8 + 2 * q + i] = -acc[rt][ct][i];
+        __syncwarp();
+        diag_factor(Dt, Mn, lane, b, logdet_acc, s_fail, s_fail_stage);
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0) *(volatile int *)&doneF[j] = 1;
+      } else {
+        spin_until(&doneF[j], 1);
+        if (type == kTaskBC) {
+          spin_until(&doneA[j * nchmax + ch], 1);
+          if (j >= 1) {
+            spin_until(&doneC[(j - 1) * nchmax + 1], 1);
+            spin_until(&doneC[(j - 1) * nchmax + ch + 1], 1);
+          }
         }
-      }
-      __syncthreads();  // diagonal factor ready, all chunks parked
-      if (tid == 0) {
-        s_chunkA = 0;
-        s_pregen = s_gen_next;  // every handed-out pre-generation task is complete here
-        s_gen_next = 0;
-        s_factored = 0;
-      }
-      // ---- phase B: solve and store every chunk
-      const int rb = (b.Cp - b.c0) >> 3;  // row tile of the border row
-      for (int ch = next_chunk(&s_chunkB, lane); ch < nch; ch = next_chunk(&s_chunkB, lane)) {
-        const int tb = 4 * ch, nv = min(4, nrt - tb);
-        if (ch == 0) {
+        __threadfence_block();
+        if (type == kTaskC0) {
 #pragma unroll
           for (int rt = 0; rt < 4; rt++)
 #pragma unroll
@@ -517,9 +560,11 @@ __global__ void __launch_bounds__(kH8Threads, MINB) k_h8(H8Args a) {
               }
         } else {
           unpark_tiles(acc, pan, tb, nv, g, q);
+          if (j >= 1) update_tiles(acc, wsb, c0, b.R, tb, nv, lane, j - 1, j);
           trsm_tiles(acc, Dt, Mn, nv, g, q);
         }
         park_tiles(acc, pan, tb, nv, g, q);
+        const int rb = (rb_abs - c0) >> 3;  // row tile of the border row
         if (rb >= tb && rb < tb + nv && g == 0) {  // border row: v^T v
 #pragma unroll
           for (int rt = 0; rt < 4; rt++)
@@ -528,15 +573,19 @@ __global__ void __launch_bounds__(kH8Threads, MINB) k_h8(H8Args a) {
               for (int ct = 0; ct < 4; ct++)
 #pragma unroll
                 for (int i = 0; i < 2; i++) {
-                  const int col = b.c0 + ct * 8 + 2 * q + i;
+                  const int col = c0 + ct * 8 + 2 * q + i;
                   if (col >= b.mt && col < b.N) quad_acc = fma(acc[rt][ct][i], acc[rt][ct][i], quad_acc);
                 }
         }
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0) {
+          *(volatile int *)&doneC[j * nchmax + ch] = 1;
+          atomicAdd(&cntC[j], 1);
+        }
       }
-      __syncthreads();  // panel j complete and visible before panel j+1 reads it
-      if (tid == 0) s_chunkB = 0;
-      if (s_fail) break;
     }
+    __syncthreads();
 
     // ---- block reduction of quad / logdet (fixed order)
 #pragma unroll
@@ -566,9 +615,20 @@ __global__ void __launch_bounds__(kH8Threads, MINB) k_h8(H8Args a) {
   }
 }
 
+static int h8_np_max(int max_N) { return (max_N + kPanel - 1) / kPanel; }
+static int h8_max_tasks(int max_N) {
+  const int np = h8_np_max(max_N), nch0 = (((np * kPanel + 8) >> 3) + 3) >> 2;
+  int n = 0;
+  for (int j = 0; j < np; j++) n += 2 * (nch0 - j) + 1;
+  return n + 4;
+}
+
 size_t h8_smem_bytes(int max_N, int d) {
-  const size_t Cp = (max_N + kPanel - 1) / kPanel * kPanel;
-  return sizeof(double) * (2 * (size_t)kPanel * kDld + 2 * SBV_MAX_D + (Cp + 8) + (size_t)max_N * d);
+  const size_t Cp = (size_t)h8_np_max(max_N) * kPanel;
+  const size_t np = h8_np_max(max_N), nch = np + 1;
+  const size_t ints = 2 * np * nch + 2 * np + ((h8_max_tasks(max_N) + 1) & ~1);
+  return sizeof(double) * (4 * (size_t)kPanel * kDld + 2 * SBV_MAX_D + (Cp + 8) + (size_t)max_N * d) +
+         sizeof(int) * ((ints + 1) & ~(size_t)1);
 }
 
 size_t h8_ws_doubles(int max_N) {
@@ -639,6 +699,8 @@ cudaError_t launch_h8(const Ctx &c, const double *theta, cudaStream_t st) {
   a.quads = c.quads;
   a.logdets = c.logdets;
   a.status = c.status;
+  a.np_max = h8_np_max(c.max_N);
+  a.max_tasks = h8_max_tasks(c.max_N);
   const double nu = theta[c.d + 1];
   cudaError_t e = cudaMemsetAsync(c.queue, 0, sizeof(unsigned int), st);
   if (e) return e;
