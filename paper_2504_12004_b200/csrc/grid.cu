@@ -1,0 +1,503 @@
+// grid.cu — exact grid-filtered nearest-anchor (RAC, H3) and m-NN (H6) search.
+//
+// The paper filters m-NN candidates with a Monte-Carlo radius lambda (Eq.7,
+// Alg.4) so that the search stays exact while touching O(alpha m)
+// points instead of O(n).  On the GPU the same idea takes the
+// form of a uniform grid over the G <= 3 scaled dimensions of largest extent:
+// cells are visited in rings of growing Chebyshev radius, every cell whose
+// lower-bound distance exceeds the current best (the nearest anchor, or the
+// m-th best neighbour) is skipped, and the search stops once the next ring's
+// lower bound exceeds it.  Candidates that survive are scored with the same
+// fma chain as the brute-force kernels (Q14) and ties are broken by
+// anchor rank / original index (Q8, Q13), so the result is bit-identical to
+// the exhaustive search; bounds carry a relative safety margin so rounding can
+// never prune a true candidate.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include <cub/cub.cuh>
+
+#include "sbv_internal.cuh"
+
+namespace sbv {
+
+// ------------------------------------------------------------------ extents
+__global__ void k_minmax_partial(const double *__restrict__ S, int64_t n, int d, double *part) {
+  __shared__ double smin[SBV_MAX_D][32], smax[SBV_MAX_D][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int j = 0; j < d; j++) {
+    double lo = INFINITY, hi = -INFINITY;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const double v = S[i * d + j];
+      lo = fmin(lo, v);
+      hi = fmax(hi, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) {
+      smin[j][w] = lo;
+      smax[j][w] = hi;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < d) {
+    const int j = threadIdx.x;
+    double lo = INFINITY, hi = -INFINITY;
+    for (int x = 0; x < (int)(blockDim.x >> 5); x++) {
+      lo = fmin(lo, smin[j][x]);
+      hi = fmax(hi, smax[j][x]);
+    }
+    part[(blockIdx.x * d + j) * 2] = lo;
+    part[(blockIdx.x * d + j) * 2 + 1] = hi;
+  }
+}
+
+cudaError_t data_extents(const double *S, int64_t n, int d, double *lo_hi_host, cudaStream_t st) {
+  const int nb = 148;
+  double *part = nullptr;
+  cudaError_t e = cudaMallocAsync(&part, sizeof(double) * nb * d * 2, st);
+  if (e) return e;
+  k_minmax_partial<<<nb, 1024, 0, st>>>(S, n, d, part);
+  std::vector<double> h(nb * d * 2);
+  e = cudaMemcpyAsync(h.data(), part, sizeof(double) * nb * d * 2, cudaMemcpyDeviceToHost, st);
+  if (e) return e;
+  e = cudaStreamSynchronize(st);
+  cudaFreeAsync(part, st);
+  if (e) return e;
+  for (int j = 0; j < d; j++) {
+    double lo = INFINITY, hi = -INFINITY;
+    for (int b = 0; b < nb; b++) {
+      lo = std::min(lo, h[(b * d + j) * 2]);
+      hi = std::max(hi, h[(b * d + j) * 2 + 1]);
+    }
+    lo_hi_host[2 * j] = lo;
+    lo_hi_host[2 * j + 1] = hi;
+  }
+  return cudaSuccess;
+}
+
+// Grid over the G <= 3 dimensions of largest extent, about `per_cell` items
+// per cell on average for `count` items.
+GridDesc make_grid(const double *lo_hi, int d, int64_t count, double per_cell) {
+  GridDesc g{};
+  int order[SBV_MAX_D];
+  for (int j = 0; j < d; j++) order[j] = j;
+  std::sort(order, order + d, [&](int a, int b) {
+    const double ea = lo_hi[2 * a + 1] - lo_hi[2 * a], eb = lo_hi[2 * b + 1] - lo_hi[2 * b];
+    return ea > eb || (ea == eb && a < b);
+  });
+  g.G = std::min(3, d);
+  // drop trailing dimensions whose extent is negligible next to the first one
+  const double e0 = lo_hi[2 * order[0] + 1] - lo_hi[2 * order[0]];
+  while (g.G > 1 && (lo_hi[2 * order[g.G - 1] + 1] - lo_hi[2 * order[g.G - 1]]) < 0.05 * e0) g.G--;
+  double vol = 1.0;
+  for (int x = 0; x < g.G; x++) {
+    g.dim[x] = order[x];
+    g.lo[x] = lo_hi[2 * order[x]];
+    const double ext = lo_hi[2 * order[x] + 1] - g.lo[x];
+    vol *= std::max(ext, 1e-300);
+  }
+  const double cells_wanted = std::max(1.0, std::min((double)count / per_cell, 4.0e6));
+  double h = std::pow(vol / cells_wanted, 1.0 / g.G);
+  if (!(h > 0) || !std::isfinite(h)) h = 1.0;
+  int64_t total = 1;
+  for (int x = 0; x < g.G; x++) {
+    const double ext = lo_hi[2 * g.dim[x] + 1] - g.lo[x];
+    g.h[x] = h;
+    g.nc[x] = (int)std::max<double>(1.0, std::min(std::ceil(ext / h) + (ext == 0 ? 1.0 : 0.0), (double)(1 << 20)));
+    g.stride[x] = (int)total;
+    total *= g.nc[x];
+  }
+  g.ncells = total;
+  return g;
+}
+
+__device__ __forceinline__ int cell_coord(double v, double lo, double h, int nc) {
+  const int c = (int)floor((v - lo) / h);
+  return min(max(c, 0), nc - 1);
+}
+
+__global__ void k_cell_ids(const double *__restrict__ S, const int32_t *__restrict__ rows,
+                           int64_t count, int d, GridDesc g, int32_t *__restrict__ cell,
+                           int32_t *__restrict__ idx) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = rows ? rows[i] : i;
+    int c = 0;
+    for (int x = 0; x < g.G; x++)
+      c += cell_coord(S[row * d + g.dim[x]], g.lo[x], g.h[x], g.nc[x]) * g.stride[x];
+    cell[i] = c;
+    idx[i] = (int32_t)i;
+  }
+}
+
+// start[c] = first sorted position whose cell >= c (empty cells share starts)
+__global__ void k_cell_starts(const int32_t *__restrict__ sorted_cell, int64_t count, int64_t ncells,
+                              int32_t *__restrict__ start) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p <= count;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = p == 0 ? -1 : sorted_cell[p - 1];
+    const int64_t b = p == count ? ncells : sorted_cell[p];
+    for (int64_t c = a + 1; c <= b; c++) start[c] = (int32_t)p;
+  }
+}
+
+// Bucket `count` items (rows of S, optionally through `rows`) into the grid:
+// list = item indices sorted by (cell, index), start = ncells + 1 offsets.
+cudaError_t build_cells(const double *S, const int32_t *rows, int64_t count, int d, const GridDesc &g,
+                        int32_t *start, int32_t *list, cudaStream_t st) {
+  int32_t *cell = nullptr, *cell_sorted = nullptr, *idx = nullptr;
+  void *tmp = nullptr;
+  size_t tmp_bytes = 0;
+  cudaError_t e;
+  if ((e = cudaMallocAsync(&cell, count * 4, st))) return e;
+  if ((e = cudaMallocAsync(&cell_sorted, count * 4, st))) return e;
+  if ((e = cudaMallocAsync(&idx, count * 4, st))) return e;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, 148 * 16));
+  k_cell_ids<<<grid, 256, 0, st>>>(S, rows, count, d, g, cell, idx);
+  int bits = 1;
+  while ((int64_t(1) << bits) < g.ncells) bits++;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, cell, cell_sorted, idx, list, (int)count, 0,
+                                  bits, st);
+  if ((e = cudaMallocAsync(&tmp, tmp_bytes, st))) return e;
+  if ((e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, cell, cell_sorted, idx, list, (int)count, 0,
+                                           bits, st)))
+    return e;
+  const int grid2 = (int)std::max<int64_t>(1, std::min<int64_t>((count + 256) / 256, 148 * 16));
+  k_cell_starts<<<grid2, 256, 0, st>>>(cell_sorted, count, g.ncells, start);
+  cudaFreeAsync(tmp, st);
+  cudaFreeAsync(cell, st);
+  cudaFreeAsync(cell_sorted, st);
+  cudaFreeAsync(idx, st);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ ring search helpers
+struct RingQ {
+  double x[3];  // query coordinates in the grid dims
+  int cq[3];    // query cell coords
+};
+
+__device__ __forceinline__ double cell_lb2(const GridDesc &g, const RingQ &q, const int (&cc)[3]) {
+  double s = 0.0;
+  for (int x = 0; x < g.G; x++) {
+    const double slack = 1e-9 * g.h[x];
+    const double clo = g.lo[x] + cc[x] * g.h[x] - slack, chi = g.lo[x] + (cc[x] + 1) * g.h[x] + slack;
+    double gap = 0.0;
+    if (cc[x] > 0 && q.x[x] < clo) gap = clo - q.x[x];
+    if (cc[x] < g.nc[x] - 1 && q.x[x] > chi) gap = q.x[x] - chi;
+    s = fma(gap, gap, s);
+  }
+  return s;
+}
+
+// squared lower bound of every cell outside the ring block of radius r; returns
+// -1 when the block already covers the whole grid
+__device__ __forceinline__ double ring_lb2(const GridDesc &g, const RingQ &q, int r) {
+  double best = INFINITY;
+  bool any = false;
+  for (int x = 0; x < g.G; x++) {
+    const double slack = 1e-9 * g.h[x];
+    if (q.cq[x] - r > 0) {
+      any = true;
+      best = fmin(best, fmax(0.0, q.x[x] - (g.lo[x] + (q.cq[x] - r) * g.h[x]) - slack));
+    }
+    if (q.cq[x] + r < g.nc[x] - 1) {
+      any = true;
+      best = fmin(best, fmax(0.0, (g.lo[x] + (q.cq[x] + r + 1) * g.h[x]) - q.x[x] - slack));
+    }
+  }
+  return any ? best * best : -1.0;
+}
+
+// prune test: can a cell / ring with squared lower bound lb2 still hold a key
+// not larger than `thr` (the current best)?  Margin absorbs rounding.
+__device__ __forceinline__ bool may_hold(double lb2, double thr) {
+  return !(lb2 > thr * (1.0 + 1e-10) + 1e-300);
+}
+
+// visit cells with Chebyshev distance exactly r (clipped to the grid); f(cell_index, lb2)
+template <class F>
+__device__ __forceinline__ void for_ring(const GridDesc &g, const RingQ &q, int r, F &&f) {
+  const int G = g.G;
+  const int r1 = G > 1 ? r : 0, r2 = G > 2 ? r : 0;
+  for (int o2 = -r2; o2 <= r2; o2++) {
+    const int c2 = G > 2 ? q.cq[2] + o2 : 0;
+    if (G > 2 && (c2 < 0 || c2 >= g.nc[2])) continue;
+    for (int o1 = -r1; o1 <= r1; o1++) {
+      const int c1 = G > 1 ? q.cq[1] + o1 : 0;
+      if (G > 1 && (c1 < 0 || c1 >= g.nc[1])) continue;
+      const bool edge = (abs(o1) == r) || (abs(o2) == r);
+      const int step = edge ? 1 : 2 * r;  // interior rows: only the two ends of dim 0
+      for (int o0 = -r; o0 <= r; o0 += (step == 0 ? 1 : step)) {
+        const int c0 = q.cq[0] + o0;
+        if (c0 < 0 || c0 >= g.nc[0]) continue;
+        const int cc[3] = {c0, c1, c2};
+        const int idx = c0 * g.stride[0] + (G > 1 ? c1 * g.stride[1] : 0) + (G > 2 ? c2 * g.stride[2] : 0);
+        f(idx, cell_lb2(g, q, cc));
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ H3 RAC
+template <int DM>
+__global__ void __launch_bounds__(256) k_rac_grid(const double *__restrict__ S, int64_t n, int d,
+                                                  const int32_t *__restrict__ anchors, GridDesc g,
+                                                  const int32_t *__restrict__ a_start,
+                                                  const int32_t *__restrict__ a_list,
+                                                  int32_t *__restrict__ block_of) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double p[DM];
+#pragma unroll
+  for (int j = 0; j < DM; j++) p[j] = j < d ? S[i * d + j] : 0.0;
+  RingQ q;
+  for (int x = 0; x < 3; x++) {
+    q.x[x] = x < g.G ? S[i * d + g.dim[x]] : 0.0;
+    q.cq[x] = x < g.G ? cell_coord(q.x[x], g.lo[x], g.h[x], g.nc[x]) : 0;
+  }
+  double best = INFINITY;
+  int32_t arg = INT32_MAX;
+  for (int r = 0;; r++) {
+    for_ring(g, q, r, [&](int cell, double lb2) {
+      if (!may_hold(lb2, best)) return;
+      for (int e = a_start[cell]; e < a_start[cell + 1]; e++) {
+        const int32_t rank = a_list[e];
+        const double *s = S + (int64_t)anchors[rank] * d;
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < DM; j++)
+          if (j < d) {
+            const double t = p[j] - s[j];
+            acc = __fma_rn(t, t, acc);
+          }
+        if (acc < best || (acc == best && rank < arg)) {  // Alg.3 argmin, ties -> lowest rank
+          best = acc;
+          arg = rank;
+        }
+      }
+    });
+    const double lb = ring_lb2(g, q, r);
+    if (lb < 0.0) break;
+    if (arg != INT32_MAX && !may_hold(lb, best)) break;
+  }
+  block_of[i] = arg;
+}
+
+cudaError_t launch_rac_grid(const double *S, int64_t n, int d, const int32_t *anchors, const GridDesc &g,
+                            const int32_t *a_start, const int32_t *a_list, int32_t *block_of,
+                            cudaStream_t st) {
+  const int grid = (int)((n + 255) / 256);
+  if (d <= 4)
+    k_rac_grid<4><<<grid, 256, 0, st>>>(S, n, d, anchors, g, a_start, a_list, block_of);
+  else if (d <= 8)
+    k_rac_grid<8><<<grid, 256, 0, st>>>(S, n, d, anchors, g, a_start, a_list, block_of);
+  else if (d <= 16)
+    k_rac_grid<16><<<grid, 256, 0, st>>>(S, n, d, anchors, g, a_start, a_list, block_of);
+  else if (d <= 32)
+    k_rac_grid<32><<<grid, 256, 0, st>>>(S, n, d, anchors, g, a_start, a_list, block_of);
+  else
+    k_rac_grid<64><<<grid, 256, 0, st>>>(S, n, d, anchors, g, a_start, a_list, block_of);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ H6 kNN
+// One warp per query block t.  Candidates = points of the cells visited whose
+// block-major position is < off_t (each cell lists positions ascending, so the
+// admissible ones are a prefix).  Keys (dist2, original index) below the
+// current m-th best are appended to a per-warp shared-memory buffer that is
+// bitonic-sorted and cut to m whenever it fills.
+constexpr int kKnnWarps = 4;
+constexpr int kKnnWcap = 1024;
+
+struct WCand {
+  double d2;
+  int32_t orig;
+  int32_t pos;
+};
+
+__device__ __forceinline__ bool wless(double da, int32_t ia, double db, int32_t ib) {
+  return da < db || (da == db && ia < ib);
+}
+
+// warp-level bitonic sort of buf[0, cnt) padded with sentinels to a power of two
+__device__ void warp_bitonic(WCand *buf, int cnt, int lane) {
+  int P = 1;
+  while (P < cnt) P <<= 1;
+  for (int i = cnt + lane; i < P; i += 32) {
+    buf[i].d2 = INFINITY;
+    buf[i].orig = INT32_MAX;
+    buf[i].pos = -1;
+  }
+  __syncwarp();
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = lane; i < P / 2; i += 32) {
+        const int lo = 2 * stride * (i / stride) + (i % stride), hi = lo + stride;
+        const bool up = ((lo & size) == 0);
+        const WCand a = buf[lo], b = buf[hi];
+        if (wless(b.d2, b.orig, a.d2, a.orig) == up) {
+          buf[lo] = b;
+          buf[hi] = a;
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+template <int DM>
+__global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
+    const double *__restrict__ Sperm, const int32_t *__restrict__ perm,
+    const int64_t *__restrict__ off, const double *__restrict__ C,
+    const int32_t *__restrict__ local_blocks, int64_t k_local, int d, int m, GridDesc g,
+    const int32_t *__restrict__ c_start, const int32_t *__restrict__ c_list, int32_t *__restrict__ nbr,
+    int32_t *__restrict__ cnt_out) {
+  extern __shared__ WCand sbuf[];  // kKnnWarps x kKnnWcap
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t li = blockIdx.x * (int64_t)kKnnWarps + w;
+  if (li >= k_local) return;
+  WCand *buf = sbuf + w * kKnnWcap;
+  const int64_t t = local_blocks[li];
+  const int32_t A = (int32_t)off[t];  // admissible positions [0, A)
+  double c[DM];
+#pragma unroll
+  for (int j = 0; j < DM; j++) c[j] = j < d ? C[t * d + j] : 0.0;
+  RingQ q;
+  for (int x = 0; x < 3; x++) {
+    q.x[x] = x < g.G ? C[t * d + g.dim[x]] : 0.0;
+    q.cq[x] = x < g.G ? cell_coord(q.x[x], g.lo[x], g.h[x], g.nc[x]) : 0;
+  }
+  int count = 0;
+  double thr_d = INFINITY;
+  int32_t thr_i = INT32_MAX;
+  int seen = 0;  // admissible points seen (for the "fewer than m exist" exit)
+  auto compact = [&]() {
+    __syncwarp();
+    warp_bitonic(buf, count, lane);
+    count = min(count, m);
+    if (count == m) {
+      thr_d = buf[m - 1].d2;
+      thr_i = buf[m - 1].orig;
+    }
+    __syncwarp();
+  };
+  // Short prefixes (the first blocks in zeta order) are scanned directly: the
+  // grid would have to sweep most of the domain to find m sparse neighbours.
+  if (A > 0 && m > 0 && A <= max(16384, 32 * m)) {
+    for (int base = 0; base < A; base += 32) {
+      const int32_t pos = base + lane;
+      const bool adm = pos < A;
+      double acc = INFINITY;
+      int32_t o = INT32_MAX;
+      if (adm) {
+        const double *s = Sperm + (int64_t)pos * d;
+        acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < DM; j++)
+          if (j < d) {
+            const double tt = c[j] - s[j];
+            acc = __fma_rn(tt, tt, acc);
+          }
+        o = perm[pos];
+      }
+      const bool ins = adm && wless(acc, o, thr_d, thr_i);
+      const unsigned mask = __ballot_sync(0xffffffffu, ins);
+      if (ins) {
+        const int slot = count + __popc(mask & ((1u << lane) - 1));
+        buf[slot].d2 = acc;
+        buf[slot].orig = o;
+        buf[slot].pos = pos;
+      }
+      count += __popc(mask);
+      if (count > kKnnWcap - 32) compact();
+    }
+  } else if (A > 0 && m > 0) {
+    for (int r = 0;; r++) {
+      for_ring(g, q, r, [&](int cell, double lb2) {
+        if (count >= m && !may_hold(lb2, thr_d)) return;
+        const int e0 = c_start[cell], e1 = c_start[cell + 1];
+        for (int base = e0; base < e1; base += 32) {
+          const int e = base + lane;
+          int32_t pos = e < e1 ? c_list[e] : INT32_MAX;
+          const bool adm = pos < A;
+          double acc = INFINITY;
+          int32_t o = INT32_MAX;
+          if (adm) {
+            const double *s = Sperm + (int64_t)pos * d;
+            acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < DM; j++)
+              if (j < d) {
+                const double tt = c[j] - s[j];
+                acc = __fma_rn(tt, tt, acc);
+              }
+            o = perm[pos];
+          }
+          const bool ins = adm && wless(acc, o, thr_d, thr_i);
+          const unsigned mask = __ballot_sync(0xffffffffu, ins);
+          const unsigned amask = __ballot_sync(0xffffffffu, adm);
+          seen += __popc(amask);
+          if (ins) {
+            const int slot = count + __popc(mask & ((1u << lane) - 1));
+            buf[slot].d2 = acc;
+            buf[slot].orig = o;
+            buf[slot].pos = pos;
+          }
+          count += __popc(mask);
+          if (count > kKnnWcap - 32) compact();
+          if (__ballot_sync(0xffffffffu, e < e1 && !adm)) break;  // rest of the cell is inadmissible
+        }
+      });
+      const double lb = ring_lb2(g, q, r);
+      if (lb < 0.0) break;
+      if (count >= m) {
+        compact();
+        if (!may_hold(lb, thr_d)) break;
+      }
+    }
+  }
+  compact();
+  const int keep = min(count, min(m, A));
+  for (int j = lane; j < m; j += 32) nbr[li * m + j] = j < keep ? buf[j].pos : -1;
+  if (lane == 0) cnt_out[li] = keep;
+  (void)seen;
+}
+
+cudaError_t launch_knn_grid(const double *Sperm, const int32_t *perm, const int64_t *off,
+                            const double *C, const int32_t *local_blocks, int64_t k_local, int d,
+                            int m, const GridDesc &g, const int32_t *c_start, const int32_t *c_list,
+                            int32_t *nbr, int32_t *cnt, cudaStream_t st) {
+  if (k_local == 0) return cudaSuccess;
+  if (m == 0) return cudaMemsetAsync(cnt, 0, k_local * 4, st);
+  const int grid = (int)((k_local + kKnnWarps - 1) / kKnnWarps);
+  const int thr = 32 * kKnnWarps;
+  const int smem = (int)(sizeof(WCand) * kKnnWarps * kKnnWcap);
+#define SBV_KNN(DMv)                                                                                    \
+  do {                                                                                                  \
+    cudaFuncSetAttribute(k_knn_grid<DMv>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);          \
+    k_knn_grid<DMv><<<grid, thr, smem, st>>>(Sperm, perm, off, C, local_blocks, k_local, d, m, g,     \
+                                             c_start, c_list, nbr, cnt);                               \
+  } while (0)
+  if (d <= 4)
+    SBV_KNN(4);
+  else if (d <= 8)
+    SBV_KNN(8);
+  else if (d <= 16)
+    SBV_KNN(16);
+  else if (d <= 32)
+    SBV_KNN(32);
+  else
+    SBV_KNN(64);
+#undef SBV_KNN
+  return cudaGetLastError();
+}
+
+int knn_grid_max_m() { return kKnnWcap - 64; }
+
+}  // namespace sbv

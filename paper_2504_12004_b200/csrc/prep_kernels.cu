@@ -139,6 +139,11 @@ __global__ void k_anchor_own_block(const int32_t *anchors, int64_t k, int32_t *b
     block_of[anchors[r]] = (int32_t)r;  // an anchor belongs to its own block
 }
 
+cudaError_t anchor_own_block(const int32_t *anchors, int64_t k, int32_t *block_of, cudaStream_t st) {
+  k_anchor_own_block<<<(int)((k + 255) / 256), 256, 0, st>>>(anchors, k, block_of);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_rac(const double *S, int64_t n, int d, const int32_t *anchors, int64_t k,
                        int32_t *block_of, cudaStream_t st) {
   int grid = (int)((n + 255) / 256);

@@ -6,6 +6,7 @@
 // only validates arguments, sizes buffers, builds the block shard / work
 // order from the device-computed layout, and launches.
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -100,6 +101,10 @@ void free_state(sbv_ctx *h) {
   release(h->result);
   release(h->queue);
   release(h->flag);
+  release(h->a_start);
+  release(h->a_list);
+  release(h->p_start);
+  release(h->p_list);
   release(h->ws);
   h->cap.clear();
   h->prepared = false;
@@ -265,6 +270,10 @@ int sbv_create(const sbv_opts *opts, sbv_handle *out) {
   }
   sbv_ctx *h = new sbv_ctx();
   cudaGetDevice(&h->device);
+  {
+    const char *e = getenv("SBV_GRID");
+    h->use_grid = (e && atoi(e) == 0) ? 0 : 1;
+  }
   if (opts) {
     h->seed = opts->seed;
     h->stream = (cudaStream_t)opts->stream;
@@ -365,7 +374,19 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   CU(select_anchors(n, k, h->seed, h->anchors, nullptr, 0, st, nullptr));
   tm.mark("H2_anchors");
   CU(ensure(h->block_of, n, unused));
-  CU(launch_rac(h->S, n, d, h->anchors, k, h->block_of, st));
+  double lo_hi[2 * SBV_MAX_D];
+  if (h->use_grid) {
+    CU(data_extents(h->S, n, d, lo_hi, st));  // one small D2H (grid geometry)
+    tm.mark("extents");
+    const GridDesc ga = make_grid(lo_hi, d, k, 3.0);
+    CU(ensure(h->a_start, ga.ncells + 1, unused));
+    CU(ensure(h->a_list, k, unused));
+    CU(build_cells(h->S, h->anchors, k, d, ga, h->a_start, h->a_list, st));
+    CU(launch_rac_grid(h->S, n, d, h->anchors, ga, h->a_start, h->a_list, h->block_of, st));
+    CU(anchor_own_block(h->anchors, k, h->block_of, st));
+  } else {
+    CU(launch_rac(h->S, n, d, h->anchors, k, h->block_of, st));
+  }
   tm.mark("H3_rac");
   CU(ensure(h->perm, n, unused));
   CU(ensure(h->off, k + 1, unused));
@@ -393,8 +414,18 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   const int mm = m > 0 ? m : 1;
   CU(ensure(h->nbr, h->k_local * mm, unused));
   CU(ensure(h->cnt, h->k_local, unused));
-  CU(launch_knn(h->Sperm, h->perm, h->off, h->C, h->local_blocks, h->k_local, d, m, h->nbr,
-                h->cnt, st));
+  if (h->use_grid && m <= knn_grid_max_m()) {
+    const GridDesc gp = make_grid(lo_hi, d, n, std::max(8.0, m / 8.0));
+    CU(ensure(h->p_start, gp.ncells + 1, unused));
+    CU(ensure(h->p_list, n, unused));
+    CU(build_cells(h->Sperm, nullptr, n, d, gp, h->p_start, h->p_list, st));
+    tm.mark("H6_grid");
+    CU(launch_knn_grid(h->Sperm, h->perm, h->off, h->C, h->local_blocks, h->k_local, d, m, gp,
+                       h->p_start, h->p_list, h->nbr, h->cnt, st));
+  } else {
+    CU(launch_knn(h->Sperm, h->perm, h->off, h->C, h->local_blocks, h->k_local, d, m, h->nbr,
+                  h->cnt, st));
+  }
   tm.mark("H6_knn");
 
   // realised sizes -> LPT work order, statistics, H8 launch geometry

@@ -58,6 +58,9 @@ struct Ctx {
   double *chunk_all = nullptr;    // world * n_chunks_local_pad x 4
   double *result = nullptr;       // 8 doubles: ell, quad, logdet, npts, nfail, fail_block, fail_stage, -
   double *result_host = nullptr;  // pinned 8 doubles
+  int32_t *a_start = nullptr, *a_list = nullptr;  // anchor grid (RAC)
+  int32_t *p_start = nullptr, *p_list = nullptr;  // point grid over block-major positions (kNN)
+  int use_grid = 1;                               // SBV_GRID=0 forces the brute-force kernels
   int *flag = nullptr;            // device: non-finite input flag
   int *flag_host = nullptr;       // pinned mirror
   unsigned int *queue = nullptr;  // work counter
@@ -76,6 +79,30 @@ struct Ctx {
   double t_prep[kMaxStages] = {}, t_llh[kMaxStages] = {};
   const char *name_prep[kMaxStages] = {}, *name_llh[kMaxStages] = {};
 };
+
+// ---- grid-filtered exact search (grid.cu)
+struct GridDesc {
+  int G;          // grid dimensions (<= 3): the scaled dims of largest extent
+  int dim[3];     // which input dimensions
+  double lo[3];   // data minimum per grid dim
+  double h[3];    // cell edge per grid dim
+  int nc[3];      // cells per grid dim
+  int stride[3];  // linear cell index strides
+  int64_t ncells;
+};
+cudaError_t data_extents(const double *S, int64_t n, int d, double *lo_hi_host, cudaStream_t st);
+GridDesc make_grid(const double *lo_hi, int d, int64_t count, double per_cell);
+cudaError_t build_cells(const double *S, const int32_t *rows, int64_t count, int d, const GridDesc &g,
+                        int32_t *start, int32_t *list, cudaStream_t st);
+cudaError_t launch_rac_grid(const double *S, int64_t n, int d, const int32_t *anchors, const GridDesc &g,
+                            const int32_t *a_start, const int32_t *a_list, int32_t *block_of,
+                            cudaStream_t st);
+cudaError_t launch_knn_grid(const double *Sperm, const int32_t *perm, const int64_t *off,
+                            const double *C, const int32_t *local_blocks, int64_t k_local, int d,
+                            int m, const GridDesc &g, const int32_t *c_start, const int32_t *c_list,
+                            int32_t *nbr, int32_t *cnt, cudaStream_t st);
+int knn_grid_max_m();
+cudaError_t anchor_own_block(const int32_t *anchors, int64_t k, int32_t *block_of, cudaStream_t st);
 
 // ---- prepare kernels (prep_kernels.cu)
 cudaError_t launch_scale(const double *X, int64_t n, int d, const double *scale_host, double *S,
