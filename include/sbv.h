@@ -74,6 +74,12 @@ void sbv_destroy(sbv_handle h);
  * the path is one ncclAllGather of the per-chunk partial sums (Alg.1
  * Step 5), which keeps ell bit-identical for every world size. */
 int sbv_comm_unique_id(void *id128);
+
+/* Host-only (no device needed): the zeta ids of the blocks rank `rank` of
+ * `world` owns, ascending: 64-block chunks c = rank, rank + world, ...
+ * blocks may be NULL (count only); capacity must be >= bc/world + 64.
+ * Errors: SBV_ERR_ARG. */
+int sbv_shard_blocks(int64_t bc, int32_t rank, int32_t world, int32_t *blocks, int64_t *count);
 int sbv_comm_init(sbv_handle h, const void *nccl_unique_id, int32_t rank, int32_t world);
 
 /* ---------------------------------------------------------------- prepare */

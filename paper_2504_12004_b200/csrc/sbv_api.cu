@@ -260,6 +260,19 @@ extern "C" {
 
 int sbv_abi_version(void) { return SBV_ABI_VERSION; }
 
+int sbv_shard_blocks(int64_t bc, int32_t rank, int32_t world, int32_t *blocks, int64_t *count) {
+  if (bc < 0 || world < 1 || rank < 0 || rank >= world || !count) return SBV_ERR_ARG;
+  const int64_t nch = (bc + kChunkBlocks - 1) / kChunkBlocks;
+  int64_t n = 0;
+  for (int64_t c = rank; c < nch; c += world)
+    for (int64_t t = c * kChunkBlocks; t < std::min<int64_t>(bc, (c + 1) * kChunkBlocks); t++) {
+      if (blocks) blocks[n] = (int32_t)t;
+      n++;
+    }
+  *count = n;
+  return SBV_OK;
+}
+
 int sbv_create(const sbv_opts *opts, sbv_handle *out) {
   if (!out) return SBV_ERR_ARG;
   *out = nullptr;
@@ -400,11 +413,12 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
 
   // shard: 64-block chunks of zeta order dealt round-robin over ranks
   h->n_chunks = (k + kChunkBlocks - 1) / kChunkBlocks;
-  std::vector<int32_t> local;
-  local.reserve(k / h->world + kChunkBlocks);
-  for (int64_t c = h->rank; c < h->n_chunks; c += h->world)
-    for (int64_t t = c * kChunkBlocks; t < std::min<int64_t>(k, (c + 1) * kChunkBlocks); t++)
-      local.push_back((int32_t)t);
+  std::vector<int32_t> local(k / h->world + kChunkBlocks + 1);
+  {
+    int64_t cnt_local = 0;
+    sbv_shard_blocks(k, h->rank, h->world, local.data(), &cnt_local);
+    local.resize(cnt_local);
+  }
   h->k_local = (int64_t)local.size();
   h->n_chunks_local = (h->k_local + kChunkBlocks - 1) / kChunkBlocks;
   CU(ensure(h->local_blocks, h->k_local, unused));

@@ -39,6 +39,7 @@ class SBVError(RuntimeError):
 _lib = None
 
 EXPORTS = ["sbv_abi_version", "sbv_create", "sbv_destroy", "sbv_comm_unique_id", "sbv_comm_init",
+           "sbv_shard_blocks",
            "sbv_prepare_h", "sbv_prepare_ex", "sbv_prepare", "sbv_loglik", "sbv_loglik_parts",
            "sbv_block_terms", "sbv_num_blocks", "sbv_get_anchors", "sbv_get_blocks",
            "sbv_get_neighbors", "sbv_stats", "sbv_stage_times", "sbv_last_error"]
@@ -57,6 +58,7 @@ def lib():
         L.sbv_destroy.restype = None
         L.sbv_comm_unique_id.argtypes = [_p]
         L.sbv_comm_init.argtypes = [_p, _p, _i32, _i32]
+        L.sbv_shard_blocks.argtypes = [_i64, _i32, _i32, _p, ctypes.POINTER(_i64)]
         L.sbv_prepare_h.argtypes = [_p, _p, _i64, _i32, _i32, _i32, _p]
         L.sbv_prepare_ex.argtypes = [_p, _i64, _i32, _i32, _i32, _p, ctypes.POINTER(sbv_opts),
                                      ctypes.POINTER(_p)]
@@ -95,6 +97,17 @@ def _f64(a):
             raise SBVError(SBV_ERR_ARG, "expected float64 tensor")
         return a.contiguous()
     return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def shard_blocks(bc: int, rank: int, world: int):
+    """Zeta ids of the blocks owned by `rank` (host-only; sbv_shard_blocks)."""
+    cnt = _i64(0)
+    rc = lib().sbv_shard_blocks(bc, rank, world, None, ctypes.byref(cnt))
+    if rc:
+        raise SBVError(rc, "sbv_shard_blocks")
+    out = np.empty(max(cnt.value, 1), dtype=np.int32)
+    lib().sbv_shard_blocks(bc, rank, world, out.ctypes.data_as(_p), ctypes.byref(cnt))
+    return out[:cnt.value].copy()
 
 
 def comm_unique_id() -> bytes:
