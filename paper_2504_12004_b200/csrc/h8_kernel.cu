@@ -47,6 +47,7 @@ namespace sbv {
 constexpr int kH8Threads = 256;
 constexpr int kH8Warps = kH8Threads / 32;
 constexpr int kDld = kPanel + 1;  // diagonal tile leading dimension (bank skew)
+constexpr int kMaxPanels = 128;   // N_t <= 4096
 
 struct H8Args {
   const double *Xp;      // n x d block-major ORIGINAL inputs
@@ -286,7 +287,8 @@ __device__ __forceinline__ void trsm_tiles(double (&acc)[4][4][2], const double 
 // Dt: in = tile (+P), out = L_jj (+ 1/L_ii in column 32);
 // Mn: out = -inv(L_ss) on the four diagonal 8x8 blocks (zero above).
 __device__ __forceinline__ void diag_factor(double *Dt, double *Mn, int lane, const BlockCtx &b,
-                                            double &logdet_acc, int &s_fail, int &s_fail_stage) {
+                                            double *logdet_slot, int &s_fail, int &s_fail_stage) {
+  double lsum = 0.0;  // this lane's log L_ii over the four sub-blocks (fixed order)
   const int g = lane >> 2, q = lane & 3;
   const int r8 = lane & 7;
 #pragma unroll 1
@@ -325,7 +327,7 @@ __device__ __forceinline__ void diag_factor(double *Dt, double *Mn, int lane, co
     }
     if (lane < 8) {
       const int col = b.c0 + o + lane;
-      if (col >= b.mt && col < b.N) logdet_acc += log(l_own);
+      if (col >= b.mt && col < b.N) lsum += log(l_own);
 #pragma unroll
       for (int j = 0; j < 8; j++) Dt[(o + lane) * kDld + o + j] = j <= lane ? a[j] : 0.0;
       Dt[(o + lane) * kDld + kPanel] = rd_own;
@@ -373,6 +375,9 @@ __device__ __forceinline__ void diag_factor(double *Dt, double *Mn, int lane, co
     }
     __syncwarp();
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+  if (lane == 0) *logdet_slot = lsum;
 }
 
 // ---------------------------------------------------------------------------
@@ -406,7 +411,7 @@ template <int NU2, int MINB>
 __global__ void __launch_bounds__(kH8Threads, MINB) k_h8(H8Args a) {
   extern __shared__ double smem[];
   __shared__ int s_item, s_fail, s_fail_stage, s_task, s_ntask;
-  __shared__ double s_red[2 * kH8Warps];
+  __shared__ double s_qp[kMaxPanels], s_lp[kMaxPanels];  // per-panel v^T v / log det parts
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int d = a.d;
@@ -489,7 +494,6 @@ __global__ void __launch_bounds__(kH8Threads, MINB) k_h8(H8Args a) {
     }
     __syncthreads();
 
-    double quad_acc = 0.0, logdet_acc = 0.0;
     const int ntask = s_ntask;
     const int rb_abs = b.Cp;  // border row index
     for (;;) {
@@ -534,7 +538,7 @@ __global__ void __launch_bounds__(kH8Threads, MINB) k_h8(H8Args a) {
 #pragma unroll
             for (int i = 0; i < 2; i++) Dt[(rt * 8 + g) * kDld + ct * 8 + 2 * q + i] = -acc[rt][ct][i];
         __syncwarp();
-        diag_factor(Dt, Mn, lane, b, logdet_acc, s_fail, s_fail_stage);
+        diag_factor(Dt, Mn, lane, b, &s_lp[j], s_fail, s_fail_stage);
         __syncwarp();
         __threadfence_block();
         if (lane == 0) *(volatile int *)&doneF[j] = 1;
@@ -565,17 +569,25 @@ __global__ void __launch_bounds__(kH8Threads, MINB) k_h8(H8Args a) {
         }
         park_tiles(acc, pan, tb, nv, g, q);
         const int rb = (rb_abs - c0) >> 3;  // row tile of the border row
-        if (rb >= tb && rb < tb + nv && g == 0) {  // border row: v^T v
+        if (rb >= tb && rb < tb + nv) {       // border row: this panel's part of v^T v
+          double qp = 0.0;
+          if (g == 0) {
 #pragma unroll
-          for (int rt = 0; rt < 4; rt++)
-            if (tb + rt == rb)
+            for (int rt = 0; rt < 4; rt++)
+              if (tb + rt == rb)
 #pragma unroll
-              for (int ct = 0; ct < 4; ct++)
+                for (int ct = 0; ct < 4; ct++)
 #pragma unroll
-                for (int i = 0; i < 2; i++) {
-                  const int col = c0 + ct * 8 + 2 * q + i;
-                  if (col >= b.mt && col < b.N) quad_acc = fma(acc[rt][ct][i], acc[rt][ct][i], quad_acc);
-                }
+                  for (int i = 0; i < 2; i++) {
+                    const int col = c0 + ct * 8 + 2 * q + i;
+                    if (col >= b.mt && col < b.N) qp = fma(acc[rt][ct][i], acc[rt][ct][i], qp);
+                  }
+          }
+          // fixed tree over lanes, one slot per panel: independent of which
+          // warp ran the task, so the block term is deterministic
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) qp += __shfl_xor_sync(0xffffffffu, qp, o);
+          if (lane == 0) s_qp[j] = qp;
         }
         __syncwarp();
         __threadfence_block();
@@ -587,22 +599,12 @@ __global__ void __launch_bounds__(kH8Threads, MINB) k_h8(H8Args a) {
     }
     __syncthreads();
 
-    // ---- block reduction of quad / logdet (fixed order)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      quad_acc += __shfl_xor_sync(0xffffffffu, quad_acc, o);
-      logdet_acc += __shfl_xor_sync(0xffffffffu, logdet_acc, o);
-    }
-    if (lane == 0) {
-      s_red[warp] = quad_acc;
-      s_red[kH8Warps + warp] = logdet_acc;
-    }
-    __syncthreads();
+    // ---- block term: per-panel parts summed in panel order (fixed)
     if (tid == 0) {
       double qs = 0.0, ls = 0.0;
-      for (int w = 0; w < kH8Warps; w++) {
-        qs += s_red[w];
-        ls += s_red[kH8Warps + w];
+      for (int j = 0; j < NP; j++) {
+        qs += s_qp[j];
+        ls += s_lp[j];
       }
       ls *= 2.0;
       const double term = -0.5 * (qs + ls) - 0.5 * (double)bst * 1.8378770664093454836;  // log 2pi

@@ -498,6 +498,7 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   h->h8_smem = h8_smem_bytes(std::max(h->max_N, 1), d);
   int smem_optin = 0;
   CU(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+  if (h->max_N > 4096) return fail(h, SBV_ERR_UNSUPPORTED, "m + block size > 4096");
   if (h->h8_smem + 1024 > (size_t)smem_optin)
     return fail(h, SBV_ERR_UNSUPPORTED, "block + neighbour set too large for shared memory staging");
   int per_sm = h8_max_ctas_per_sm(h->h8_smem);

@@ -52,10 +52,16 @@ def main():
             merged[owned] = all_terms[r][owned]
             mn[owned] = all_nbr[r][0][owned]
             mc[owned] = all_nbr[r][1][owned]
-        print(f"ll world={world}: {ll_w!r}  ll 1-GPU: {ll_1!r}")
-        ok &= ll_w == ll_1
-        ok &= bool(np.array_equal(merged, terms_1))
-        ok &= bool(np.array_equal(mn, nbr_1)) and bool(np.array_equal(mc, cnt_1))
+        checks = {"ll": ll_w == ll_1, "terms": bool(np.array_equal(merged, terms_1)),
+                  "nbr": bool(np.array_equal(mn, nbr_1)), "cnt": bool(np.array_equal(mc, cnt_1))}
+        print(f"ll world={world}: {ll_w!r}  ll 1-GPU: {ll_1!r}  checks: {checks}")
+        if not checks["terms"]:
+            bad = np.where(merged != terms_1)[0]
+            print("terms differ at", bad[:10], merged[bad[:5]], terms_1[bad[:5]])
+        if not checks["nbr"]:
+            bad = np.where((mn != nbr_1).any(1))[0]
+            print("nbr differ at", bad[:10], mn[bad[0]][:8], nbr_1[bad[0]][:8])
+        ok = all(checks.values())
         print("MGPU_OK" if ok else "MGPU_FAIL")
     dist.barrier()
     dist.destroy_process_group()
