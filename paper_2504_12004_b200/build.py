@@ -15,7 +15,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libsbv.so")
+LIB = os.environ.get("SBV_LIB_OUT") or os.path.join(HERE, "libsbv.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -51,7 +51,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     inc, libdir = nccl_paths()
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+    extra = os.environ.get("SBV_NVCC_EXTRA", "").split()  # experiments only
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", *extra,
            "-I", os.path.join(ROOT, "include"), "-I", inc,
            *sources(), "-o", LIB + ".tmp",
            "-L", libdir, "-l:libnccl.so.2", f"-Xlinker=-rpath={libdir}"]

@@ -141,10 +141,39 @@ __device__ __forceinline__ int pan_off(int lr, int c) {
 // the upper triangle of the diagonal tile is skipped.
 template <int NU2>
 __device__ __forceinline__ void gen_chunk(double *pan, const BlockCtx &b, int tb, int nv, int lane) {
+#ifdef SBV_EXP_NOGEN  // timing ablation only
+  for (int rr = 0; rr < 8 * nv; rr++) pan[pan_off(tb * 8 + rr, lane)] = (b.c0 + tb * 8 + rr == b.c0 + lane) ? -1.0 : 0.0;
+  return;
+#endif
   const int c = b.c0 + lane;
   const double *xc = b.vs + (size_t)min(c, b.N - 1) * b.d;
+  int rr = 0;
+  {
+    // two rows per iteration (two independent Matérn chains for ILP); rows
+    // past N fall through to the generic loop below
 #pragma unroll 1
-  for (int rr = 0; rr < 8 * nv; rr++) {
+    for (; rr + 1 < 8 * nv && b.c0 + tb * 8 + rr + 1 < b.N; rr += 2) {
+      const int lr = tb * 8 + rr, r0 = b.c0 + lr;
+      const double *x0 = b.vs + (size_t)r0 * b.d, *x1 = x0 + b.d;
+      double s0 = 0.0, s1 = 0.0;
+      for (int jj = 0; jj < b.d; jj++) {  // Eq.5
+        const double xj = xc[jj];
+        const double u0 = x0[jj] - xj, u1 = x1[jj] - xj;
+        s0 = fma(u0, u0, s0);
+        s1 = fma(u1, u1, s1);
+      }
+      double v0 = neg_matern<NU2>(sqrt(s0), b.msigma2);
+      double v1 = neg_matern<NU2>(sqrt(s1), b.msigma2);
+      if (r0 == c) v0 += b.mtau2;  // nugget on the diagonal only (Q3)
+      if (r0 + 1 == c) v1 += b.mtau2;
+      if (!(c <= r0 && c < b.N)) v0 = 0.0;
+      if (!(c <= r0 + 1 && c < b.N)) v1 = 0.0;
+      pan[pan_off(lr, lane)] = v0;
+      pan[pan_off(lr + 1, lane)] = v1;
+    }
+  }
+#pragma unroll 1
+  for (; rr < 8 * nv; rr++) {
     const int lr = tb * 8 + rr, r = b.c0 + lr;
     double v = 0.0;
     if (r < b.N && c <= r && c < b.N) {
@@ -165,11 +194,63 @@ __device__ __forceinline__ void gen_chunk(double *pan, const BlockCtx &b, int tb
   }
 }
 
+// phase A (1'): the same -covariance generated straight into the DMMA
+// accumulators (row = lane/4, cols 2(lane%4)+{0,1}).  The row-tile loop is
+// rolled (8 inlined Matérn evaluations, not 32: the kernel stays inside the
+// I-cache) and the accumulator tiles rotate through the loop so every
+// register index stays compile-time.
+template <int NU2>
+__device__ __forceinline__ void gen_tiles(double (&acc)[4][4][2], const BlockCtx &b, int tb, int nv,
+                                          int g, int q) {
+#pragma unroll 1
+  for (int rt = 0; rt < 4; rt++) {
+    const int r = b.c0 + (tb + rt) * 8 + g;
+    const bool real_r = rt < nv && r < b.N;
+    const double *xr = b.vs + (size_t)min(r, b.N - 1) * b.d;
+    double t[4][2];
+#pragma unroll
+    for (int ct = 0; ct < 4; ct++)
+#pragma unroll
+      for (int i = 0; i < 2; i++) {
+        const int c = b.c0 + ct * 8 + 2 * q + i;
+        double v = 0.0;
+        if (real_r && c < b.N && c <= r) {
+          const double *xc = b.vs + (size_t)c * b.d;
+          double s = 0.0;
+          for (int jj = 0; jj < b.d; jj++) {  // Eq.5
+            const double u = xr[jj] - xc[jj];
+            s = fma(u, u, s);
+          }
+          v = neg_matern<NU2>(sqrt(s), b.msigma2);
+          if (r == c) v += b.mtau2;  // nugget on the diagonal only (Q3)
+        } else if (rt < nv) {
+          if (r == b.Cp)
+            v = -b.ys[c];  // border row
+          else if (r == c)
+            v = -1.0;  // identity padding (r >= N)
+        }
+        t[ct][i] = v;
+      }
+#pragma unroll
+    for (int ct = 0; ct < 4; ct++)
+#pragma unroll
+      for (int i = 0; i < 2; i++) {
+        acc[0][ct][i] = acc[1][ct][i];
+        acc[1][ct][i] = acc[2][ct][i];
+        acc[2][ct][i] = acc[3][ct][i];
+        acc[3][ct][i] = t[ct][i];
+      }
+  }
+}
+
 // phase A (2): acc += L[rows, 0:c0] L[c0:c0+32, 0:c0]^T on DMMA, operands from
 // the workspace (L2), 8 k-steps per previous panel, 2-stage prefetch.
 // Only previous panels [p0, p1) are applied (update-ahead splits the range).
 __device__ __forceinline__ void update_tiles(double (&acc)[4][4][2], const double *wsb, int c0,
                                              int R, int tb, int nv, int lane, int p0, int p1) {
+#ifdef SBV_EXP_NOUPDATE  // timing ablation only
+  return;
+#endif
   if (p1 <= p0 || nv == 0) return;
   // Row tiles past nv (a chunk's ragged tail) read the last valid row tile and
   // their results are never stored: the DMMA stream stays unpredicated.
@@ -252,6 +333,9 @@ __device__ __forceinline__ double c_to_a(const double (&t)[2], int g, int q, int
 // Dt holds L_jj, Mn holds -inv(L_ss) on the diagonal 8x8 blocks.
 __device__ __forceinline__ void trsm_tiles(double (&acc)[4][4][2], const double *Dt, const double *Mn,
                                            int nv, int g, int q) {
+#ifdef SBV_EXP_NOTRSM  // timing ablation only
+  return;
+#endif
 #pragma unroll
   for (int rt = 0; rt < 4; rt++) {
     if (rt < nv) {
@@ -514,6 +598,11 @@ __global__ void __launch_bounds__(kH8Threads, MINB) k_h8(H8Args a) {
       if (type == kTaskA) {
         if (j >= 2) spin_until(&cntC[j - 2], nch0 - (j - 2));
         __threadfence_block();
+#ifdef SBV_GEN_IN_REGS  // measured slower (cfg2 22.5 vs 14.5 ms): kept for reference
+        gen_tiles<NU2>(acc, b, tb, nv, g, q);
+        if (j >= 2) update_tiles(acc, wsb, c0, b.R, tb, nv, lane, 0, j - 1);
+        park_tiles(acc, pan, tb, nv, g, q);
+#else
         gen_chunk<NU2>(pan, b, tb, nv, lane);
         if (j >= 2) {
           __syncwarp();
@@ -521,6 +610,7 @@ __global__ void __launch_bounds__(kH8Threads, MINB) k_h8(H8Args a) {
           update_tiles(acc, wsb, c0, b.R, tb, nv, lane, 0, j - 1);
           park_tiles(acc, pan, tb, nv, g, q);
         }
+#endif
         __syncwarp();
         __threadfence_block();
         if (lane == 0) *(volatile int *)&doneA[j * nchmax + ch] = 1;
@@ -538,21 +628,18 @@ __global__ void __launch_bounds__(kH8Threads, MINB) k_h8(H8Args a) {
 #pragma unroll
             for (int i = 0; i < 2; i++) Dt[(rt * 8 + g) * kDld + ct * 8 + 2 * q + i] = -acc[rt][ct][i];
         __syncwarp();
+#ifndef SBV_EXP_NOFACTOR
         diag_factor(Dt, Mn, lane, b, &s_lp[j], s_fail, s_fail_stage);
+#else  // timing experiment only: skip the diagonal factorisation (wrong results)
+        if (lane == 0) s_lp[j] = 0.0;
+#endif
         __syncwarp();
         __threadfence_block();
         if (lane == 0) *(volatile int *)&doneF[j] = 1;
       } else {
-        spin_until(&doneF[j], 1);
-        if (type == kTaskBC) {
-          spin_until(&doneA[j * nchmax + ch], 1);
-          if (j >= 1) {
-            spin_until(&doneC[(j - 1) * nchmax + 1], 1);
-            spin_until(&doneC[(j - 1) * nchmax + ch + 1], 1);
-          }
-        }
-        __threadfence_block();
         if (type == kTaskC0) {
+          spin_until(&doneF[j], 1);
+          __threadfence_block();
 #pragma unroll
           for (int rt = 0; rt < 4; rt++)
 #pragma unroll
@@ -563,6 +650,13 @@ __global__ void __launch_bounds__(kH8Threads, MINB) k_h8(H8Args a) {
                 acc[rt][ct][i] = cc <= rr ? Dt[rr * kDld + cc] : 0.0;
               }
         } else {
+          spin_until(&doneF[j], 1);
+          spin_until(&doneA[j * nchmax + ch], 1);
+          if (j >= 1) {
+            spin_until(&doneC[(j - 1) * nchmax + 1], 1);
+            spin_until(&doneC[(j - 1) * nchmax + ch + 1], 1);
+          }
+          __threadfence_block();
           unpark_tiles(acc, pan, tb, nv, g, q);
           if (j >= 1) update_tiles(acc, wsb, c0, b.R, tb, nv, lane, j - 1, j);
           trsm_tiles(acc, Dt, Mn, nv, g, q);

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsbv.so")
+LIB_PATH = os.environ.get("SBV_LIB") or os.path.join(HERE, "libsbv.so")
 
 SBV_OK, SBV_ERR_ARG, SBV_ERR_CUDA, SBV_ERR_OOM, SBV_ERR_NOT_PD, SBV_ERR_UNSUPPORTED, \
     SBV_ERR_COMM, SBV_ERR_STATE = range(8)
