@@ -246,12 +246,13 @@ __device__ __forceinline__ void for_ring(const GridDesc &g, const RingQ &q, int 
 
 // ------------------------------------------------------------------ H3 RAC
 template <int DM>
-__global__ void __launch_bounds__(256) k_rac_grid(const double *__restrict__ S, int64_t n, int d,
+__global__ void __launch_bounds__(256) k_rac_grid(const double *__restrict__ S, int64_t n, int64_t i0, int d,
                                                   const int32_t *__restrict__ anchors, GridDesc g,
                                                   const int32_t *__restrict__ a_start,
                                                   const int32_t *__restrict__ a_list,
                                                   int32_t *__restrict__ block_of) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  // points [i0, n); block_of is indexed relative to i0 (one rank's slice)
+  const int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   double p[DM];
 #pragma unroll
@@ -286,23 +287,24 @@ __global__ void __launch_bounds__(256) k_rac_grid(const double *__restrict__ S, 
     if (lb < 0.0) break;
     if (arg != INT32_MAX && !may_hold(lb, best)) break;
   }
-  block_of[i] = arg;
+  block_of[i - i0] = arg;
 }
 
-cudaError_t launch_rac_grid(const double *S, int64_t n, int d, const int32_t *anchors, const GridDesc &g,
+cudaError_t launch_rac_grid(const double *S, int64_t n, int64_t i0, int d, const int32_t *anchors, const GridDesc &g,
                             const int32_t *a_start, const int32_t *a_list, int32_t *block_of,
                             cudaStream_t st) {
-  const int grid = (int)((n + 255) / 256);
+  if (n <= i0) return cudaSuccess;
+  const int grid = (int)((n - i0 + 255) / 256);
   if (d <= 4)
-    k_rac_grid<4><<<grid, 256, 0, st>>>(S, n, d, anchors, g, a_start, a_list, block_of);
+    k_rac_grid<4><<<grid, 256, 0, st>>>(S, n, i0, d, anchors, g, a_start, a_list, block_of);
   else if (d <= 8)
-    k_rac_grid<8><<<grid, 256, 0, st>>>(S, n, d, anchors, g, a_start, a_list, block_of);
+    k_rac_grid<8><<<grid, 256, 0, st>>>(S, n, i0, d, anchors, g, a_start, a_list, block_of);
   else if (d <= 16)
-    k_rac_grid<16><<<grid, 256, 0, st>>>(S, n, d, anchors, g, a_start, a_list, block_of);
+    k_rac_grid<16><<<grid, 256, 0, st>>>(S, n, i0, d, anchors, g, a_start, a_list, block_of);
   else if (d <= 32)
-    k_rac_grid<32><<<grid, 256, 0, st>>>(S, n, d, anchors, g, a_start, a_list, block_of);
+    k_rac_grid<32><<<grid, 256, 0, st>>>(S, n, i0, d, anchors, g, a_start, a_list, block_of);
   else
-    k_rac_grid<64><<<grid, 256, 0, st>>>(S, n, d, anchors, g, a_start, a_list, block_of);
+    k_rac_grid<64><<<grid, 256, 0, st>>>(S, n, i0, d, anchors, g, a_start, a_list, block_of);
   return cudaGetLastError();
 }
 
@@ -357,12 +359,12 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
     const int64_t *__restrict__ off, const double *__restrict__ C,
     const int32_t *__restrict__ local_blocks, int64_t k_local, int d, int m, GridDesc g,
     const int32_t *__restrict__ c_start, const int32_t *__restrict__ c_list, int32_t *__restrict__ nbr,
-    int32_t *__restrict__ cnt_out) {
-  extern __shared__ WCand sbuf[];  // kKnnWarps x kKnnWcap
+    int32_t *__restrict__ cnt_out, int wcap) {
+  extern __shared__ WCand sbuf[];  // kKnnWarps x wcap
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t li = blockIdx.x * (int64_t)kKnnWarps + w;
   if (li >= k_local) return;
-  WCand *buf = sbuf + w * kKnnWcap;
+  WCand *buf = sbuf + w * wcap;
   const int64_t t = local_blocks[li];
   const int32_t A = (int32_t)off[t];  // admissible positions [0, A)
   double c[DM];
@@ -415,7 +417,7 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
         buf[slot].pos = pos;
       }
       count += __popc(mask);
-      if (count > kKnnWcap - 32) compact();
+      if (count > wcap - 32) compact();
     }
   } else if (A > 0 && m > 0) {
     for (int r = 0;; r++) {
@@ -450,14 +452,17 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
             buf[slot].pos = pos;
           }
           count += __popc(mask);
-          if (count > kKnnWcap - 32) compact();
+          if (count > wcap - 32) compact();
           if (__ballot_sync(0xffffffffu, e < e1 && !adm)) break;  // rest of the cell is inadmissible
         }
       });
       const double lb = ring_lb2(g, q, r);
       if (lb < 0.0) break;
       if (count >= m) {
-        compact();
+        // a full sort only when the threshold is unset or the buffer has
+        // grown well past m; otherwise test termination against the current
+        // (conservative) m-th best
+        if (thr_d == INFINITY || count > m + 128) compact();
         if (!may_hold(lb, thr_d)) break;
       }
     }
@@ -477,12 +482,16 @@ cudaError_t launch_knn_grid(const double *Sperm, const int32_t *perm, const int6
   if (m == 0) return cudaMemsetAsync(cnt, 0, k_local * 4, st);
   const int grid = (int)((k_local + kKnnWarps - 1) / kKnnWarps);
   const int thr = 32 * kKnnWarps;
-  const int smem = (int)(sizeof(WCand) * kKnnWarps * kKnnWcap);
+  // per-warp candidate buffer: the smallest power of two >= m + 160 (headroom
+  // between compactions) keeps shared memory low and occupancy high
+  int wcap = 1024;  // measured: 512 at m=200 costs more compactions than it gains
+  while (wcap < 2 * m + 128) wcap <<= 1;
+  const int smem = (int)(sizeof(WCand) * kKnnWarps * wcap);
 #define SBV_KNN(DMv)                                                                                    \
   do {                                                                                                  \
     cudaFuncSetAttribute(k_knn_grid<DMv>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);          \
     k_knn_grid<DMv><<<grid, thr, smem, st>>>(Sperm, perm, off, C, local_blocks, k_local, d, m, g,     \
-                                             c_start, c_list, nbr, cnt);                               \
+                                             c_start, c_list, nbr, cnt, wcap);                         \
   } while (0)
   if (d <= 4)
     SBV_KNN(4);

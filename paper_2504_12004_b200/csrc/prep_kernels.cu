@@ -83,6 +83,78 @@ cudaError_t select_anchors(int64_t n, int64_t k, uint64_t seed, int32_t *anchors
   return cudaGetLastError();
 }
 
+// Fast path: the keys are uniform 64-bit integers, so the k smallest lie below
+// T = (2k + 1024)/n * 2^64 with overwhelming probability.  Candidates below T
+// are appended, sorted by (key, index) with two small stable radix passes, and
+// the first k taken.  *bad is set when the candidate set cannot be trusted
+// (overflow, or fewer than k candidates); the caller then runs the full sort.
+__global__ void k_key_filter(int64_t n, uint64_t seed, uint64_t thr, int cap, uint64_t *ck, int32_t *ci,
+                             int *count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = splitmix64(seed, (uint64_t)i);
+    if (key < thr) {
+      const int slot = atomicAdd(count, 1);
+      if (slot < cap) {
+        ck[slot] = key;
+        ci[slot] = (int32_t)i;
+      }
+    }
+  }
+}
+
+__global__ void k_fill_sentinel(int cap, uint64_t *ck, int32_t *ci) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x) {
+    ck[i] = UINT64_MAX;
+    ci[i] = INT32_MAX;
+  }
+}
+
+__global__ void k_anchor_check(const int *count, int cap, int64_t k, int *bad) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *bad = (*count > cap || *count < k) ? 1 : 0;
+}
+
+cudaError_t select_anchors_fast(int64_t n, int64_t k, uint64_t seed, int32_t *anchors, int *bad,
+                                cudaStream_t st) {
+  const double frac = std::min(1.0, (2.0 * k + 1024.0) / (double)n);
+  if (frac >= 0.25) {  // small n: nothing to gain, signal "use the full sort"
+    cudaMemsetAsync(bad, 0xff, sizeof(int), st);
+    return cudaGetLastError();
+  }
+  const uint64_t thr = (uint64_t)(frac * 18446744073709551616.0);
+  const int cap = (int)(4 * k + 4096);
+  uint64_t *ck = nullptr, *ck2 = nullptr;
+  int32_t *ci = nullptr, *ci2 = nullptr;
+  int *count = nullptr;
+  void *tmp = nullptr;
+  size_t tb1 = 0, tb2 = 0;
+  cudaError_t e;
+  if ((e = cudaMallocAsync(&ck, cap * 8, st))) return e;
+  if ((e = cudaMallocAsync(&ck2, cap * 8, st))) return e;
+  if ((e = cudaMallocAsync(&ci, cap * 4, st))) return e;
+  if ((e = cudaMallocAsync(&ci2, cap * 4, st))) return e;
+  if ((e = cudaMallocAsync(&count, sizeof(int), st))) return e;
+  cudaMemsetAsync(count, 0, sizeof(int), st);
+  k_fill_sentinel<<<std::max(1, std::min(cap / 256 + 1, 1024)), 256, 0, st>>>(cap, ck, ci);
+  k_key_filter<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(n, seed, thr, cap, ck,
+                                                                                  ci, count);
+  k_anchor_check<<<1, 32, 0, st>>>(count, cap, k, bad);
+  // (key, index) order: stable pass on the index, then a stable pass on the key
+  cub::DeviceRadixSort::SortPairs(nullptr, tb1, ci, ci2, ck, ck2, cap, 0, 32, st);
+  cub::DeviceRadixSort::SortPairs(nullptr, tb2, ck2, ck, ci2, ci, cap, 0, 64, st);
+  if ((e = cudaMallocAsync(&tmp, std::max(tb1, tb2), st))) return e;
+  cub::DeviceRadixSort::SortPairs(tmp, tb1, ci, ci2, ck, ck2, cap, 0, 32, st);
+  cub::DeviceRadixSort::SortPairs(tmp, tb2, ck2, ck, ci2, ci, cap, 0, 64, st);
+  cudaMemcpyAsync(anchors, ci, k * 4, cudaMemcpyDeviceToDevice, st);
+  cudaFreeAsync(tmp, st);
+  cudaFreeAsync(ck, st);
+  cudaFreeAsync(ck2, st);
+  cudaFreeAsync(ci, st);
+  cudaFreeAsync(ci2, st);
+  cudaFreeAsync(count, st);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ H3
 // Squared scaled distance, the fma chain of DESIGN.md Q14.
 template <int DM>

@@ -294,7 +294,7 @@ int sbv_create(const sbv_opts *opts, sbv_handle *out) {
   }
   for (int i = 0; i <= kMaxStages; i++) cudaEventCreate(&h->ev[i]);
   if (cudaMallocHost(&h->result_host, 8 * sizeof(double)) != cudaSuccess ||
-      cudaMallocHost(&h->flag_host, sizeof(int)) != cudaSuccess) {
+      cudaMallocHost(&h->flag_host, 2 * sizeof(int)) != cudaSuccess) {
     delete h;
     return SBV_ERR_OOM;
   }
@@ -375,7 +375,7 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   CU(ensure(h->X, n * d, unused));
   CU(cudaMemcpyAsync(h->X, X, n * d * sizeof(double), cudaMemcpyDefault, st));
   // finiteness flag: read back at the first host sync below (no extra stall)
-  CU(ensure(h->flag, 1, unused));
+  CU(ensure(h->flag, 2, unused));
   CU(cudaMemsetAsync(h->flag, 0, sizeof(int), st));
   k_check_finite<<<grid_for(n * d), 256, 0, st>>>(h->X, n * d, h->flag);
   CU(cudaMemcpyAsync(h->flag_host, h->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -384,18 +384,35 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   CU(launch_scale(h->X, n, d, scale, h->S, st));
   tm.mark("H1_scale");
   CU(ensure(h->anchors, k, unused));
-  CU(select_anchors(n, k, h->seed, h->anchors, nullptr, 0, st, nullptr));
+  if (h->use_grid) {  // filtered selection; verified at the next host sync (extents)
+    CU(select_anchors_fast(n, k, h->seed, h->anchors, h->flag + 1, st));
+    CU(cudaMemcpyAsync(h->flag_host + 1, h->flag + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  } else {
+    CU(select_anchors(n, k, h->seed, h->anchors, nullptr, 0, st, nullptr));
+  }
   tm.mark("H2_anchors");
   CU(ensure(h->block_of, n, unused));
   double lo_hi[2 * SBV_MAX_D];
   if (h->use_grid) {
-    CU(data_extents(h->S, n, d, lo_hi, st));  // one small D2H (grid geometry)
+    CU(data_extents(h->S, n, d, lo_hi, st));  // one small D2H (grid geometry) + sync
+    if (h->flag_host[1] != 0) CU(select_anchors(n, k, h->seed, h->anchors, nullptr, 0, st, nullptr));
     tm.mark("extents");
     const GridDesc ga = make_grid(lo_hi, d, k, 3.0);
     CU(ensure(h->a_start, ga.ncells + 1, unused));
     CU(ensure(h->a_list, k, unused));
     CU(build_cells(h->S, h->anchors, k, d, ga, h->a_start, h->a_list, st));
-    CU(launch_rac_grid(h->S, n, d, h->anchors, ga, h->a_start, h->a_list, h->block_of, st));
+    if (h->world > 1) {
+      // RAC sharded by points: rank r assigns points [r c, (r+1) c), then one
+      // in-place allgather rebuilds block_of everywhere (NVLink, 4 B/point)
+      const int64_t chunk = (n + h->world - 1) / h->world;
+      CU(ensure(h->block_of, chunk * h->world, unused));
+      const int64_t i0 = std::min<int64_t>(n, h->rank * chunk), i1 = std::min<int64_t>(n, i0 + chunk);
+      CU(launch_rac_grid(h->S, i1, i0, d, h->anchors, ga, h->a_start, h->a_list,
+                         h->block_of + h->rank * chunk, st));
+      NC(ncclAllGather(h->block_of + h->rank * chunk, h->block_of, (size_t)chunk, ncclInt32, h->comm, st));
+    } else {
+      CU(launch_rac_grid(h->S, n, 0, d, h->anchors, ga, h->a_start, h->a_list, h->block_of, st));
+    }
     CU(anchor_own_block(h->anchors, k, h->block_of, st));
   } else {
     CU(launch_rac(h->S, n, d, h->anchors, k, h->block_of, st));
@@ -501,7 +518,11 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   if (h->max_N > 4096) return fail(h, SBV_ERR_UNSUPPORTED, "m + block size > 4096");
   if (h->h8_smem + 1024 > (size_t)smem_optin)
     return fail(h, SBV_ERR_UNSUPPORTED, "block + neighbour set too large for shared memory staging");
-  int per_sm = h8_max_ctas_per_sm(h->h8_smem);
+  if (h->h8_smem != h->occ_smem) {  // occupancy query only when the smem size changes
+    h->occ_smem = h->h8_smem;
+    h->occ_per_sm = h8_max_ctas_per_sm(h->h8_smem);
+  }
+  int per_sm = h->occ_per_sm;
   if (per_sm < 1) per_sm = 1;
   h->h8_grid = (int)std::min<int64_t>((int64_t)sms * per_sm, std::max<int64_t>(h->k_local, 1));
   h->ws_per_cta = h8_ws_doubles(std::max(h->max_N, 1));

@@ -68,6 +68,8 @@ struct Ctx {
   size_t ws_per_cta = 0;
   int h8_grid = 0;
   size_t h8_smem = 0;
+  size_t occ_smem = 0;  // cached occupancy query
+  int occ_per_sm = 0;
   std::unordered_map<void *, size_t> cap;  // device buffer capacities (bytes)
   // errors
   int64_t err_block = -1;
@@ -94,7 +96,7 @@ cudaError_t data_extents(const double *S, int64_t n, int d, double *lo_hi_host, 
 GridDesc make_grid(const double *lo_hi, int d, int64_t count, double per_cell);
 cudaError_t build_cells(const double *S, const int32_t *rows, int64_t count, int d, const GridDesc &g,
                         int32_t *start, int32_t *list, cudaStream_t st);
-cudaError_t launch_rac_grid(const double *S, int64_t n, int d, const int32_t *anchors, const GridDesc &g,
+cudaError_t launch_rac_grid(const double *S, int64_t n, int64_t i0, int d, const int32_t *anchors, const GridDesc &g,
                             const int32_t *a_start, const int32_t *a_list, int32_t *block_of,
                             cudaStream_t st);
 cudaError_t launch_knn_grid(const double *Sperm, const int32_t *perm, const int64_t *off,
@@ -109,6 +111,8 @@ cudaError_t launch_scale(const double *X, int64_t n, int d, const double *scale_
                          cudaStream_t st);
 cudaError_t select_anchors(int64_t n, int64_t k, uint64_t seed, int32_t *anchors, void *tmp,
                            size_t tmp_bytes, cudaStream_t st, size_t *tmp_needed);
+cudaError_t select_anchors_fast(int64_t n, int64_t k, uint64_t seed, int32_t *anchors, int *bad,
+                                cudaStream_t st);
 cudaError_t launch_rac(const double *S, int64_t n, int d, const int32_t *anchors, int64_t k,
                        int32_t *block_of, cudaStream_t st);
 cudaError_t build_layout(const int32_t *block_of, int64_t n, int64_t k, int32_t *perm,
