@@ -420,17 +420,68 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
       if (count > wcap - 32) compact();
     }
   } else if (A > 0 && m > 0) {
+    const int G = g.G;
     for (int r = 0;; r++) {
-      for_ring(g, q, r, [&](int cell, double lb2) {
-        if (count >= m && !may_hold(lb2, thr_d)) return;
-        const int e0 = c_start[cell], e1 = c_start[cell + 1];
-        for (int base = e0; base < e1; base += 32) {
-          const int e = base + lane;
-          int32_t pos = e < e1 ? c_list[e] : INT32_MAX;
-          const bool adm = pos < A;
+      // The ring's cells are handled 32 at a time: each lane takes one cell of
+      // the ring's bounding box, skips interior / out-of-grid / pruned cells,
+      // and binary-searches its cell's admissible prefix (positions ascending,
+      // admissible iff < A); the warp then scores the up-to-32 ranges as one
+      // flattened list.  The per-cell global loads are issued in parallel
+      // instead of one dependent chain per cell.
+      const int side = 2 * r + 1;
+      int64_t box = side;
+      if (G > 1) box *= side;
+      if (G > 2) box *= side;
+      for (int64_t b0 = 0; b0 < box; b0 += 32) {
+        const int64_t bi = b0 + lane;
+        int e_lo = 0, e_cnt = 0;
+        if (bi < box) {
+          const int o0 = (int)(bi % side) - r;
+          const int o1 = G > 1 ? (int)((bi / side) % side) - r : 0;
+          const int o2 = G > 2 ? (int)(bi / ((int64_t)side * side)) - r : 0;
+          const int cc[3] = {q.cq[0] + o0, q.cq[1] + o1, q.cq[2] + o2};
+          bool ok = max(abs(o0), max(abs(o1), abs(o2))) == r;
+          for (int x = 0; x < G; x++) ok = ok && cc[x] >= 0 && cc[x] < g.nc[x];
+          if (ok && !(count >= m && !may_hold(cell_lb2(g, q, cc), thr_d))) {
+            const int cell = cc[0] * g.stride[0] + (G > 1 ? cc[1] * g.stride[1] : 0) +
+                             (G > 2 ? cc[2] * g.stride[2] : 0);
+            const int s0 = c_start[cell], s1 = c_start[cell + 1];
+            int lo = s0, hi = s1;
+            while (lo < hi) {
+              const int mid = (lo + hi) >> 1;
+              if (c_list[mid] < A)
+                lo = mid + 1;
+              else
+                hi = mid;
+            }
+            e_lo = s0;
+            e_cnt = lo - s0;
+          }
+        }
+        int incl = e_cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        const int excl = incl - e_cnt;
+        for (int f0 = 0; f0 < total; f0 += 32) {
+          const int f = f0 + lane;
+          int owner = 0;  // largest lane whose range starts at or before f
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const int cand = owner + step;
+            const int ex = __shfl_sync(0xffffffffu, excl, min(cand, 31));
+            if (cand < 32 && ex <= f) owner = cand;
+          }
+          const int o_lo = __shfl_sync(0xffffffffu, e_lo, owner);
+          const int o_ex = __shfl_sync(0xffffffffu, excl, owner);
+          const bool adm = f < total;
+          int32_t pos = INT32_MAX, o = INT32_MAX;
           double acc = INFINITY;
-          int32_t o = INT32_MAX;
           if (adm) {
+            pos = c_list[o_lo + (f - o_ex)];
             const double *s = Sperm + (int64_t)pos * d;
             acc = 0.0;
 #pragma unroll
@@ -443,8 +494,6 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
           }
           const bool ins = adm && wless(acc, o, thr_d, thr_i);
           const unsigned mask = __ballot_sync(0xffffffffu, ins);
-          const unsigned amask = __ballot_sync(0xffffffffu, adm);
-          seen += __popc(amask);
           if (ins) {
             const int slot = count + __popc(mask & ((1u << lane) - 1));
             buf[slot].d2 = acc;
@@ -453,9 +502,8 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
           }
           count += __popc(mask);
           if (count > wcap - 32) compact();
-          if (__ballot_sync(0xffffffffu, e < e1 && !adm)) break;  // rest of the cell is inadmissible
         }
-      });
+      }
       const double lb = ring_lb2(g, q, r);
       if (lb < 0.0) break;
       if (count >= m) {

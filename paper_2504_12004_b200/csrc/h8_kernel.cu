@@ -44,8 +44,7 @@
 
 namespace sbv {
 
-constexpr int kH8Threads = 256;
-constexpr int kH8Warps = kH8Threads / 32;
+constexpr int kH8Threads = 256;  // 8 warps share one block's task graph
 constexpr int kDld = kPanel + 1;  // diagonal tile leading dimension (bank skew)
 constexpr int kMaxPanels = 128;   // N_t <= 4096
 
@@ -496,7 +495,7 @@ __global__ void __launch_bounds__(kH8Threads, MINB) k_h8(H8Args a) {
   extern __shared__ double smem[];
   __shared__ int s_item, s_fail, s_fail_stage, s_task, s_ntask;
   __shared__ double s_qp[kMaxPanels], s_lp[kMaxPanels];  // per-panel v^T v / log det parts
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
   const int d = a.d;
   const int npmax = a.np_max, nchmax = npmax + 1;
