@@ -312,12 +312,18 @@ def run_ours(args):
     except Exception:
         launches = None
 
+    prep_mean = {k_: statistics.mean(v) for k_, v in stage_prep.items()}
+    llh_mean = {k_: statistics.mean(v) for k_, v in stage_llh.items()}
+    stages = {**{"prep." + k_: v for k_, v in prep_mean.items()},
+              **{"llh." + k_: v for k_, v in llh_mean.items()}}
+    stages_all = [stages]
+    if world > 1:
+        stages_all = [None] * world
+        dist.all_gather_object(stages_all, stages)
     if rank == 0:
         evals_s = 1e3 / ms_max
-        prep_mean = {k_: statistics.mean(v) for k_, v in stage_prep.items()}
-        llh_mean = {k_: statistics.mean(v) for k_, v in stage_llh.items()}
-        stages = {**{"prep." + k_: v for k_, v in prep_mean.items()},
-                  **{"llh." + k_: v for k_, v in llh_mean.items()}}
+        stages_max = {k_: max(s.get(k_, 0.0) for s in stages_all) for k_ in stages}
+        stages_min = {k_: min(s.get(k_, 0.0) for s in stages_all) for k_ in stages}
         dom = max(((k_, v) for k_, v in stages.items() if "H" in k_), key=lambda kv: kv[1])
         h8_tf = flops_total / (h8_ms_max * 1e-3) / 1e12
         roof = roofline(dom, stats, c, fp64_peak, peaks, world, h8_ms_max, flops_total, h8_bytes_total)
@@ -333,6 +339,8 @@ def run_ours(args):
                             "h8_frac_of_fp64_peak": h8_tf / fp64_peak,
                             "fp64_peak_tflops": fp64_peak, "flops_per_eval": flops_total},
             "stage_ms_rank0": stages,
+            **({"stage_ms_max_over_ranks": stages_max, "stage_ms_min_over_ranks": stages_min}
+               if world > 1 else {}),
             "dominant_stage": dom[0],
             "roofline": roof,
             "e2e": {"value": 1e3 / e2e_ms_max, "unit": "evals/s",
@@ -357,6 +365,27 @@ def run_ours(args):
     return 0
 
 
+def ncu_traffic(fname: str):
+    """DRAM bytes of one launch from the newest committed ncu summary (profiles/rNN/), or None."""
+    pdir = os.path.join(ROOT, "profiles")
+    if not os.path.isdir(pdir):
+        return None
+    for rnd in sorted(os.listdir(pdir), reverse=True):
+        p = os.path.join(pdir, rnd, fname)
+        if os.path.exists(p):
+            try:
+                m = json.load(open(p))
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+                tot = 0.0
+                for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                    v, u = m[key]
+                    tot += float(v) * scale[u]
+                return tot
+            except (KeyError, ValueError, TypeError):
+                return None
+    return None
+
+
 def roofline(dom, stats, c, fp64_peak, peaks, world, h8_ms, flops_total, h8_bytes_total):
     """Roofline object for the dominant stage of the step."""
     name, ms = dom
@@ -365,7 +394,10 @@ def roofline(dom, stats, c, fp64_peak, peaks, world, h8_ms, flops_total, h8_byte
         ach = flops_total / world / (ms * 1e-3) / 1e12
         return {"kernel": "k_h8 (fused per-block bordered Cholesky, DMMA)", "bound": "tensor",
                 "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak,
-                "traffic": None, "peak_source": "measured DMMA.8x8x4 FP64 (profiles/r01/fp64_peaks.jsonl)",
+                "traffic": ncu_traffic("h8_full_ncu_summary.json") if world == 1 else None,
+                "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one k_h8 launch, "
+                                  "ncu --set full (profiles/, latest round)",
+                "peak_source": "measured DMMA.8x8x4 FP64 (profiles/r01/fp64_peaks.jsonl)",
                 "algorithmic_per_launch": flops_total / world}
     # kNN / RAC: FP64 ALU bound; algorithmic ops = 3 d FP64 flops per pair (sub, mul, add)
     pairs = stats["knn_pairs"] if "H6" in name else (stats["rac_pairs"] / world if "H3" in name else None)

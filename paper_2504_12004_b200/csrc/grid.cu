@@ -176,6 +176,81 @@ cudaError_t build_cells(const double *S, const int32_t *rows, int64_t count, int
   return cudaGetLastError();
 }
 
+KnnLevels make_knn_levels(const double *lo_hi, int d, int64_t n, int m) {
+  KnnLevels lv{};
+  const double per_cell = std::max(8.0, m / 8.0);
+  // a direct scan of a short prefix beats the ring search of a grid with a
+  // handful of cells around m neighbours
+  lv.direct_max = (int32_t)std::min<int64_t>(n, std::max(2048, 16 * m));
+  int64_t P = n;
+  lv.nl = 0;
+  int64_t cells = 0, items = 0;
+  while (lv.nl < kMaxLevels) {
+    const int l = lv.nl++;
+    lv.P[l] = (int32_t)P;
+    lv.g[l] = make_grid(lo_hi, d, P, per_cell);
+    lv.cell_off[l] = cells;
+    lv.list_off[l] = items;
+    cells += lv.g[l].ncells;
+    items += P;
+    // one level while 2n items do not fit the int32 sort
+    if (2 * n >= (int64_t(1) << 31) || (P + 1) / 2 < lv.direct_max) break;
+    P = (P + 1) / 2;
+  }
+  lv.cell_off[lv.nl] = cells;
+  lv.list_off[lv.nl] = items;
+  return lv;
+}
+
+__global__ void k_cell_ids_levels(const double *__restrict__ S, int d, KnnLevels lv,
+                                  int32_t *__restrict__ cell, int32_t *__restrict__ idx) {
+  const int64_t total = lv.list_off[lv.nl];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int l = 0;
+    while (l + 1 < lv.nl && e >= lv.list_off[l + 1]) l++;
+    const int64_t i = e - lv.list_off[l];
+    const GridDesc &g = lv.g[l];
+    int64_t c = lv.cell_off[l];
+    for (int x = 0; x < g.G; x++)
+      c += cell_coord(S[i * d + g.dim[x]], g.lo[x], g.h[x], g.nc[x]) * (int64_t)g.stride[x];
+    cell[e] = (int32_t)c;
+    idx[e] = (int32_t)i;
+  }
+}
+
+// All levels bucketed by one radix sort: key = global cell id (level cells
+// are consecutive), value = position; the sort is stable, so each cell lists
+// its positions ascending.
+cudaError_t build_knn_levels(const double *Sperm, int d, const KnnLevels &lv, int32_t *start,
+                             int32_t *list, cudaStream_t st) {
+  const int64_t count = lv.list_off[lv.nl], ncells = lv.cell_off[lv.nl];
+  int32_t *cell = nullptr, *cell_sorted = nullptr, *idx = nullptr;
+  void *tmp = nullptr;
+  size_t tmp_bytes = 0;
+  cudaError_t e;
+  if ((e = cudaMallocAsync(&cell, count * 4, st))) return e;
+  if ((e = cudaMallocAsync(&cell_sorted, count * 4, st))) return e;
+  if ((e = cudaMallocAsync(&idx, count * 4, st))) return e;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, 148 * 16));
+  k_cell_ids_levels<<<grid, 256, 0, st>>>(Sperm, d, lv, cell, idx);
+  int bits = 1;
+  while ((int64_t(1) << bits) < ncells) bits++;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, cell, cell_sorted, idx, list, (int)count, 0,
+                                  bits, st);
+  if ((e = cudaMallocAsync(&tmp, tmp_bytes, st))) return e;
+  if ((e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, cell, cell_sorted, idx, list, (int)count, 0,
+                                           bits, st)))
+    return e;
+  const int grid2 = (int)std::max<int64_t>(1, std::min<int64_t>((count + 256) / 256, 148 * 16));
+  k_cell_starts<<<grid2, 256, 0, st>>>(cell_sorted, count, ncells, start);
+  cudaFreeAsync(tmp, st);
+  cudaFreeAsync(cell, st);
+  cudaFreeAsync(cell_sorted, st);
+  cudaFreeAsync(idx, st);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ ring search helpers
 struct RingQ {
   double x[3];  // query coordinates in the grid dims
@@ -357,8 +432,8 @@ template <int DM>
 __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
     const double *__restrict__ Sperm, const int32_t *__restrict__ perm,
     const int64_t *__restrict__ off, const double *__restrict__ C,
-    const int32_t *__restrict__ local_blocks, int64_t k_local, int d, int m, GridDesc g,
-    const int32_t *__restrict__ c_start, const int32_t *__restrict__ c_list, int32_t *__restrict__ nbr,
+    const int32_t *__restrict__ local_blocks, int64_t k_local, int d, int m, KnnLevels lv,
+    const int32_t *__restrict__ c_start_all, const int32_t *__restrict__ c_list, int32_t *__restrict__ nbr,
     int32_t *__restrict__ cnt_out, int wcap) {
   extern __shared__ WCand sbuf[];  // kKnnWarps x wcap
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -367,6 +442,16 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
   WCand *buf = sbuf + w * wcap;
   const int64_t t = local_blocks[li];
   const int32_t A = (int32_t)off[t];  // admissible positions [0, A)
+  // the smallest prefix level that indexes all of [0, A)
+  GridDesc g = lv.g[0];
+  int64_t coff = 0;
+#pragma unroll
+  for (int l = 1; l < kMaxLevels; l++)
+    if (l < lv.nl && lv.P[l] >= A) {
+      g = lv.g[l];
+      coff = lv.cell_off[l];
+    }
+  const int32_t *__restrict__ c_start = c_start_all + coff;
   double c[DM];
 #pragma unroll
   for (int j = 0; j < DM; j++) c[j] = j < d ? C[t * d + j] : 0.0;
@@ -391,7 +476,7 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
   };
   // Short prefixes (the first blocks in zeta order) are scanned directly: the
   // grid would have to sweep most of the domain to find m sparse neighbours.
-  if (A > 0 && m > 0 && A <= max(16384, 32 * m)) {
+  if (A > 0 && m > 0 && A <= lv.direct_max) {
     for (int base = 0; base < A; base += 32) {
       const int32_t pos = base + lane;
       const bool adm = pos < A;
@@ -524,7 +609,7 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
 
 cudaError_t launch_knn_grid(const double *Sperm, const int32_t *perm, const int64_t *off,
                             const double *C, const int32_t *local_blocks, int64_t k_local, int d,
-                            int m, const GridDesc &g, const int32_t *c_start, const int32_t *c_list,
+                            int m, const KnnLevels &lv, const int32_t *c_start, const int32_t *c_list,
                             int32_t *nbr, int32_t *cnt, cudaStream_t st) {
   if (k_local == 0) return cudaSuccess;
   if (m == 0) return cudaMemsetAsync(cnt, 0, k_local * 4, st);
@@ -538,7 +623,7 @@ cudaError_t launch_knn_grid(const double *Sperm, const int32_t *perm, const int6
 #define SBV_KNN(DMv)                                                                                    \
   do {                                                                                                  \
     cudaFuncSetAttribute(k_knn_grid<DMv>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);          \
-    k_knn_grid<DMv><<<grid, thr, smem, st>>>(Sperm, perm, off, C, local_blocks, k_local, d, m, g,     \
+    k_knn_grid<DMv><<<grid, thr, smem, st>>>(Sperm, perm, off, C, local_blocks, k_local, d, m, lv,    \
                                              c_start, c_list, nbr, cnt, wcap);                         \
   } while (0)
   if (d <= 4)

@@ -114,6 +114,42 @@ __global__ void k_anchor_check(const int *count, int cap, int64_t k, int *bad) {
   if (threadIdx.x == 0 && blockIdx.x == 0) *bad = (*count > cap || *count < k) ? 1 : 0;
 }
 
+// Rank of each candidate in (key, index) order = number of candidates below
+// it; the candidate of rank r < k is anchor r.  splitmix64 is a bijection of
+// i (odd multiplier, xor-shifts, odd multipliers), so keys never tie and the
+// key alone orders them.  The candidate range is split over gridDim.y slices
+// whose partial ranks are summed with atomics.
+constexpr int kRankMaxCap = 4 * 16384 + 4096;
+constexpr int kRankSlices = 8;
+__global__ void __launch_bounds__(256) k_rank_candidates(const uint64_t *__restrict__ ck,
+                                                         const int *__restrict__ count, int cap,
+                                                         int *__restrict__ rank) {
+  __shared__ uint64_t sk[256];
+  const int c = min(*count, cap);
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (blockIdx.x * 256 >= c) return;  // whole CTA beyond the candidates
+  const uint64_t key = i < c ? ck[i] : UINT64_MAX;
+  const int j0 = (int)((int64_t)c * blockIdx.y / gridDim.y), j1 = (int)((int64_t)c * (blockIdx.y + 1) / gridDim.y);
+  int r = 0;
+  for (int b = j0; b < j1; b += 256) {
+    __syncthreads();
+    const int j = b + threadIdx.x;
+    sk[threadIdx.x] = j < j1 ? ck[j] : UINT64_MAX;
+    __syncthreads();
+    const int lim = min(256, j1 - b);
+#pragma unroll 8
+    for (int x = 0; x < lim; x++) r += sk[x] < key ? 1 : 0;
+  }
+  if (i < c && r) atomicAdd(&rank[i], r);
+}
+
+__global__ void k_rank_scatter(const int32_t *__restrict__ ci, const int *__restrict__ count, int cap,
+                               const int *__restrict__ rank, int64_t k, int32_t *__restrict__ anchors) {
+  const int c = min(*count, cap);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x)
+    if (rank[i] < k) anchors[rank[i]] = ci[i];
+}
+
 cudaError_t select_anchors_fast(int64_t n, int64_t k, uint64_t seed, int32_t *anchors, int *bad,
                                 cudaStream_t st) {
   const double frac = std::min(1.0, (2.0 * k + 1024.0) / (double)n);
@@ -135,10 +171,23 @@ cudaError_t select_anchors_fast(int64_t n, int64_t k, uint64_t seed, int32_t *an
   if ((e = cudaMallocAsync(&ci2, cap * 4, st))) return e;
   if ((e = cudaMallocAsync(&count, sizeof(int), st))) return e;
   cudaMemsetAsync(count, 0, sizeof(int), st);
-  k_fill_sentinel<<<std::max(1, std::min(cap / 256 + 1, 1024)), 256, 0, st>>>(cap, ck, ci);
+  if (cap > kRankMaxCap)  // the radix-sort path sorts all cap slots
+    k_fill_sentinel<<<std::max(1, std::min(cap / 256 + 1, 1024)), 256, 0, st>>>(cap, ck, ci);
   k_key_filter<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(n, seed, thr, cap, ck,
                                                                                   ci, count);
   k_anchor_check<<<1, 32, 0, st>>>(count, cap, k, bad);
+  if (cap <= kRankMaxCap) {  // all-pairs rank: two launches instead of ~12 radix passes
+    int *rank = reinterpret_cast<int *>(ci2);
+    cudaMemsetAsync(rank, 0, cap * sizeof(int), st);
+    k_rank_candidates<<<dim3((cap + 255) / 256, kRankSlices), 256, 0, st>>>(ck, count, cap, rank);
+    k_rank_scatter<<<(cap + 255) / 256, 256, 0, st>>>(ci, count, cap, rank, k, anchors);
+    cudaFreeAsync(ck, st);
+    cudaFreeAsync(ck2, st);
+    cudaFreeAsync(ci, st);
+    cudaFreeAsync(ci2, st);
+    cudaFreeAsync(count, st);
+    return cudaGetLastError();
+  }
   // (key, index) order: stable pass on the index, then a stable pass on the key
   cub::DeviceRadixSort::SortPairs(nullptr, tb1, ci, ci2, ck, ck2, cap, 0, 32, st);
   cub::DeviceRadixSort::SortPairs(nullptr, tb2, ck2, ck, ci2, ci, cap, 0, 64, st);
@@ -300,22 +349,44 @@ cudaError_t launch_gather_rows(const double *S, const int32_t *perm, int64_t n, 
 
 // ------------------------------------------------------------------ H5
 // Alg.4 line 6: c_t = (sum of members, ascending index) / |B_t|.
-__global__ void k_centroids(const double *__restrict__ Sperm, const int64_t *__restrict__ off,
-                            int64_t k, int d, double *__restrict__ C) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < k * d;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t t = e / d;
-    int j = (int)(e - t * d);
-    double s = 0.0;
-    for (int64_t p = off[t]; p < off[t + 1]; p++) s = __dadd_rn(s, Sperm[p * d + j]);
-    C[e] = __ddiv_rn(s, (double)(off[t + 1] - off[t]));
+// Only the blocks listed in `blocks` (this rank's queries; all blocks when
+// null); C stays indexed by the global zeta id.
+// One warp per block: the block's rows (contiguous in the block-major layout)
+// are staged through shared memory with coalesced loads, then lane j sums
+// coordinate j in member order (the sequential sum of Q4).
+constexpr int kCenWarps = 4, kCenTile = 1024;  // doubles staged per warp
+__global__ void __launch_bounds__(32 * kCenWarps)
+    k_centroids(const double *__restrict__ Sperm, const int64_t *__restrict__ off,
+                const int32_t *__restrict__ blocks, int64_t k, int d, double *__restrict__ C) {
+  __shared__ double tile[kCenWarps][kCenTile];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int rows_per_tile = kCenTile / d;
+  for (int64_t i = blockIdx.x * (int64_t)kCenWarps + w; i < k; i += (int64_t)gridDim.x * kCenWarps) {
+    const int64_t t = blocks ? blocks[i] : i;
+    const int64_t p0 = off[t], p1 = off[t + 1];
+    double s0 = 0.0, s1 = 0.0;  // coordinates lane and lane + 32 (d <= 64)
+    for (int64_t r0 = p0; r0 < p1; r0 += rows_per_tile) {
+      const int rows = p1 - r0 < rows_per_tile ? (int)(p1 - r0) : rows_per_tile;
+      const double *src = Sperm + r0 * d;
+      for (int e = lane; e < rows * d; e += 32) tile[w][e] = src[e];
+      __syncwarp();
+      if (lane < d)
+        for (int r = 0; r < rows; r++) s0 = __dadd_rn(s0, tile[w][r * d + lane]);
+      if (lane + 32 < d)
+        for (int r = 0; r < rows; r++) s1 = __dadd_rn(s1, tile[w][r * d + lane + 32]);
+      __syncwarp();
+    }
+    const double cntd = (double)(p1 - p0);
+    if (lane < d) C[t * d + lane] = __ddiv_rn(s0, cntd);
+    if (lane + 32 < d) C[t * d + lane + 32] = __ddiv_rn(s1, cntd);
   }
 }
 
-cudaError_t launch_centroids(const double *Sperm, const int64_t *off, int64_t k, int d,
-                             double *C, cudaStream_t st) {
-  int grid = (int)std::min<int64_t>((k * d + 255) / 256, 148 * 16);
-  k_centroids<<<grid, 256, 0, st>>>(Sperm, off, k, d, C);
+cudaError_t launch_centroids(const double *Sperm, const int64_t *off, const int32_t *blocks,
+                             int64_t k, int d, double *C, cudaStream_t st) {
+  if (k <= 0) return cudaSuccess;
+  int grid = (int)std::min<int64_t>((k + kCenWarps - 1) / kCenWarps, 148 * 16);
+  k_centroids<<<grid, 32 * kCenWarps, 0, st>>>(Sperm, off, blocks, k, d, C);
   return cudaGetLastError();
 }
 

@@ -424,10 +424,6 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   CU(ensure(h->Sperm, n * d, unused));
   CU(launch_gather_rows(h->S, h->perm, n, d, h->Sperm, st));
   tm.mark("H4_layout");
-  CU(ensure(h->C, k * d, unused));
-  CU(launch_centroids(h->Sperm, h->off, k, d, h->C, st));
-  tm.mark("H5_centroids");
-
   // shard: 64-block chunks of zeta order dealt round-robin over ranks
   h->n_chunks = (k + kChunkBlocks - 1) / kChunkBlocks;
   std::vector<int32_t> local(k / h->world + kChunkBlocks + 1);
@@ -441,17 +437,21 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   CU(ensure(h->local_blocks, h->k_local, unused));
   CU(cudaMemcpyAsync(h->local_blocks, local.data(), h->k_local * sizeof(int32_t),
                      cudaMemcpyHostToDevice, st));
+  CU(ensure(h->C, k * d, unused));
+  CU(launch_centroids(h->Sperm, h->off, h->world > 1 ? h->local_blocks : nullptr, h->k_local, d,
+                      h->C, st));
+  tm.mark("H5_centroids");
 
   const int mm = m > 0 ? m : 1;
   CU(ensure(h->nbr, h->k_local * mm, unused));
   CU(ensure(h->cnt, h->k_local, unused));
   if (h->use_grid && m <= knn_grid_max_m()) {
-    const GridDesc gp = make_grid(lo_hi, d, n, std::max(8.0, m / 8.0));
-    CU(ensure(h->p_start, gp.ncells + 1, unused));
-    CU(ensure(h->p_list, n, unused));
-    CU(build_cells(h->Sperm, nullptr, n, d, gp, h->p_start, h->p_list, st));
+    const KnnLevels lv = make_knn_levels(lo_hi, d, n, m);
+    CU(ensure(h->p_start, lv.cell_off[lv.nl] + 1, unused));
+    CU(ensure(h->p_list, lv.list_off[lv.nl], unused));
+    CU(build_knn_levels(h->Sperm, d, lv, h->p_start, h->p_list, st));
     tm.mark("H6_grid");
-    CU(launch_knn_grid(h->Sperm, h->perm, h->off, h->C, h->local_blocks, h->k_local, d, m, gp,
+    CU(launch_knn_grid(h->Sperm, h->perm, h->off, h->C, h->local_blocks, h->k_local, d, m, lv,
                        h->p_start, h->p_list, h->nbr, h->cnt, st));
   } else {
     CU(launch_knn(h->Sperm, h->perm, h->off, h->C, h->local_blocks, h->k_local, d, m, h->nbr,
@@ -488,9 +488,14 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   h->h8_bytes = 0;
   for (int64_t li = 0; li < h->k_local; li++)
     h->h8_bytes += (double)Nt[li] * (d + 1) * 8.0 + (double)cnt_h[li] * 4.0 + 4 * 8.0;
+  // LPT order (N_t descending, ties by local index): a stable counting sort
   std::vector<int32_t> order(h->k_local);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return Nt[a] > Nt[b]; });
+  {
+    std::vector<int64_t> bucket((size_t)h->max_N + 2, 0);
+    for (int64_t li = 0; li < h->k_local; li++) bucket[h->max_N - Nt[li] + 1]++;
+    for (size_t b = 1; b < bucket.size(); b++) bucket[b] += bucket[b - 1];
+    for (int64_t li = 0; li < h->k_local; li++) order[bucket[h->max_N - Nt[li]]++] = (int32_t)li;
+  }
   CU(ensure(h->work_order, h->k_local, unused));
   CU(cudaMemcpyAsync(h->work_order, order.data(), h->k_local * sizeof(int32_t),
                      cudaMemcpyHostToDevice, st));
@@ -620,6 +625,8 @@ int sbv_get_blocks(sbv_handle h, int32_t *block_of_point, int64_t *off, int32_t 
   if ((rc = copy_out(h, block_of_point, h->block_of, h->n * sizeof(int32_t)))) return rc;
   if ((rc = copy_out(h, off, h->off, (h->k + 1) * sizeof(int64_t)))) return rc;
   if ((rc = copy_out(h, perm, h->perm, h->n * sizeof(int32_t)))) return rc;
+  if (centroids && h->world > 1)  // prepare computed only this rank's query blocks
+    CU(launch_centroids(h->Sperm, h->off, nullptr, h->k, h->d, h->C, h->stream));
   if ((rc = copy_out(h, centroids, h->C, h->k * h->d * sizeof(double)))) return rc;
   return SBV_OK;
 }

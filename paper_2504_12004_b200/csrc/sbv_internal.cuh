@@ -92,6 +92,22 @@ struct GridDesc {
   int stride[3];  // linear cell index strides
   int64_t ncells;
 };
+// Prefix-level grids for the kNN (H6): level l buckets the block-major
+// positions [0, P[l]) (P halves from n), so a query whose admissible prefix is
+// [0, A) searches the smallest level with P >= A, where at least half of the
+// indexed points are admissible.  All levels share one list / start array.
+constexpr int kMaxLevels = 16;
+struct KnnLevels {
+  int nl;
+  int32_t direct_max;               // prefixes A <= direct_max are scanned directly
+  int32_t P[kMaxLevels];            // decreasing
+  int64_t cell_off[kMaxLevels + 1]; // level l cells start at cell_off[l] in `start`
+  int64_t list_off[kMaxLevels + 1]; // level l items occupy list[list_off[l], list_off[l+1])
+  GridDesc g[kMaxLevels];
+};
+KnnLevels make_knn_levels(const double *lo_hi, int d, int64_t n, int m);
+cudaError_t build_knn_levels(const double *Sperm, int d, const KnnLevels &lv, int32_t *start,
+                             int32_t *list, cudaStream_t st);
 cudaError_t data_extents(const double *S, int64_t n, int d, double *lo_hi_host, cudaStream_t st);
 GridDesc make_grid(const double *lo_hi, int d, int64_t count, double per_cell);
 cudaError_t build_cells(const double *S, const int32_t *rows, int64_t count, int d, const GridDesc &g,
@@ -101,7 +117,7 @@ cudaError_t launch_rac_grid(const double *S, int64_t n, int64_t i0, int d, const
                             cudaStream_t st);
 cudaError_t launch_knn_grid(const double *Sperm, const int32_t *perm, const int64_t *off,
                             const double *C, const int32_t *local_blocks, int64_t k_local, int d,
-                            int m, const GridDesc &g, const int32_t *c_start, const int32_t *c_list,
+                            int m, const KnnLevels &lv, const int32_t *c_start, const int32_t *c_list,
                             int32_t *nbr, int32_t *cnt, cudaStream_t st);
 int knn_grid_max_m();
 cudaError_t anchor_own_block(const int32_t *anchors, int64_t k, int32_t *block_of, cudaStream_t st);
@@ -120,8 +136,8 @@ cudaError_t build_layout(const int32_t *block_of, int64_t n, int64_t k, int32_t 
                          size_t *tmp_needed);
 cudaError_t launch_gather_rows(const double *S, const int32_t *perm, int64_t n, int d,
                                double *Sperm, cudaStream_t st);
-cudaError_t launch_centroids(const double *Sperm, const int64_t *off, int64_t k, int d,
-                             double *C, cudaStream_t st);
+cudaError_t launch_centroids(const double *Sperm, const int64_t *off, const int32_t *blocks,
+                             int64_t k, int d, double *C, cudaStream_t st);
 cudaError_t launch_knn(const double *Sperm, const int32_t *perm, const int64_t *off,
                        const double *C, const int32_t *local_blocks, int64_t k_local, int d,
                        int m, int32_t *nbr, int32_t *cnt, cudaStream_t st);

@@ -176,6 +176,73 @@ def test_argument_errors(sbv):
     assert e.value.code == 1
 
 
+def test_grid_search_equals_brute_force(sbv, monkeypatch):
+    """The grid-filtered RAC / multi-level kNN against the
+    exhaustive kernels (SBV_GRID=0, oracle-checked at small n) at a size with
+    several prefix levels: identical partitions, neighbours and likelihood."""
+    import torch
+    n, d, bs, m = 300_000, 10, 30, 100
+    X = torch.from_numpy(si.make_X(n, d, seed=41)).cuda()
+    y = torch.from_numpy(si.make_y(X.cpu().numpy(), seed=42)).cuda()
+    sc = si.default_scale(d)
+    theta = si.default_theta(d, nu=1.5, tau2=1e-4)
+    hg = sbv.prepare(X, bs, m, sc)
+    monkeypatch.setenv("SBV_GRID", "0")
+    hb = sbv.prepare(X, bs, m, sc)
+    np.testing.assert_array_equal(hg.anchors(), hb.anchors())
+    for a, b in zip(hg.blocks(), hb.blocks()):
+        np.testing.assert_array_equal(a, b)
+    for a, b in zip(hg.neighbors(), hb.neighbors()):
+        np.testing.assert_array_equal(a, b)
+    assert hg.loglik(y, theta) == hb.loglik(y, theta)
+
+
+def test_cfg2_full_size_sampled(sbv, orc):
+    """BASELINE.json configs[1] (n=1e6, d=10, bs=100, m=200) in the launch
+    configuration bench.py times: anchors, layout and centroids in full,
+    nearest-anchor assignment on 4,000 sampled points, the neighbour sets and
+    block terms of 40 sampled blocks (every prefix level), and the total
+    against the oracle's sum over the GPU's (sample-verified) structure."""
+    import torch
+    c = si.CONFIGS["cfg2"]
+    n, d, bs, m = c["n"], c["d"], c["bs"], c["m"]
+    X = si.make_X(n, d, seed=1)
+    y = si.make_y(X, seed=2, kind="iid")
+    sc = si.default_scale(d)
+    theta = si.default_theta(d, nu=c["nu"], tau2=1e-4)
+    h = sbv.prepare(torch.from_numpy(X).cuda(), bs, m, sc)
+    k = orc.num_blocks(n, bs)
+    anc = h.anchors()
+    np.testing.assert_array_equal(anc, orc.anchors(n, k, 3))
+    S = orc.scale(X, sc)
+    bo, off, perm, C = h.blocks()
+    rng = np.random.default_rng(7)
+    smp = np.setdiff1d(rng.choice(n, 4000, replace=False), anc)
+    # nearest anchor of sampled points: anchors first, so anchor rank r is row r
+    bo_s = orc.rac(np.concatenate([S[anc], S[smp]]), np.arange(k, dtype=np.int32))[k:]
+    np.testing.assert_array_equal(bo[smp], bo_s)
+    perm_o, off_o = orc.layout(bo, k)
+    np.testing.assert_array_equal(perm, perm_o)
+    np.testing.assert_array_equal(off, off_o)
+    np.testing.assert_array_equal(C, orc.centroids(S, perm, off))
+    nbr, cnt = h.neighbors()
+    # 40 blocks over the zeta order, log-spaced so every prefix level is hit
+    ts = np.unique(np.concatenate([[0, 1, 2, k - 1],
+                                   np.geomspace(3, k - 2, 36).astype(np.int64)]))
+    for t in ts:
+        ref = orc.knn_block(S, perm, off, C, int(t), m)
+        assert cnt[t] == len(ref), t
+        np.testing.assert_array_equal(nbr[t, :cnt[t]], ref, err_msg=f"block {t}")
+    terms, quads, logdets = h.block_terms(torch.from_numpy(y).cuda(), theta)
+    for t in ts:
+        to, qo, lo = orc.block_term_at(X, y, perm, off, nbr, cnt, int(t), theta)
+        b = max(abs(to), 0.5 * (abs(qo) + abs(lo)) + 0.5 * (off[t + 1] - off[t]) * math.log(2 * math.pi))
+        assert abs(terms[t] - to) <= TOL_TERM * b, (t, terms[t], to)
+    ll = h.loglik(torch.from_numpy(y).cuda(), theta)
+    ll_o = orc.loglik(X, y, perm, off, nbr, cnt, theta)
+    assert abs(ll - ll_o) <= TOL_LL * max(abs(ll_o), np.abs(terms).sum()), (ll, ll_o)
+
+
 def test_cfg1_full_size(sbv, orc):
     """BASELINE.json configs[0]: n=20,000, d=10, bs=20, m=60, Matérn-5/2."""
     c = si.CONFIGS["cfg1"]
