@@ -52,13 +52,32 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     inc, libdir = nccl_paths()
     extra = os.environ.get("SBV_NVCC_EXTRA", "").split()  # experiments only
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", *extra,
-           "-I", os.path.join(ROOT, "include"), "-I", inc,
-           *sources(), "-o", LIB + ".tmp",
-           "-L", libdir, "-l:libnccl.so.2", f"-Xlinker=-rpath={libdir}"]
+    objdir = os.path.join(os.path.dirname(LIB), "_obj")
+    os.makedirs(objdir, exist_ok=True)
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *extra,
+             "-I", os.path.join(ROOT, "include"), "-I", inc]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd))
+        flags.insert(0, "-Xptxas=-v")
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [NVCC, *flags, "-c", src, "-o", obj]
+        if verbose:
+            print(" ".join(cmd))
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, r
+
+    # translation units compile in parallel (the H8 variants dominate)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        results = list(ex.map(compile_one, sources()))
+    for src, _, r in results:
+        if verbose or r.returncode:
+            sys.stderr.write(r.stdout + r.stderr)
+        if r.returncode:
+            raise subprocess.CalledProcessError(r.returncode, f"nvcc -c {src}")
+    cmd = [NVCC, *ARCH, "-shared", *[o for _, o, _ in results], "-o", LIB + ".tmp",
+           "-L", libdir, "-l:libnccl.so.2", f"-Xlinker=-rpath={libdir}"]
     subprocess.run(cmd, check=True)
     os.replace(LIB + ".tmp", LIB)
     return LIB

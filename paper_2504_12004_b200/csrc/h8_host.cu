@@ -1,0 +1,111 @@
+// h8_host.cu — host side of H8 (h8_kernel.cuh): workspace / shared-memory
+// sizing, occupancy, variant selection and launch.
+#include "h8_kernel.cuh"
+
+namespace sbv {
+
+static int h8_np_max(int max_N) { return (max_N + kPanel - 1) / kPanel; }
+static int h8_max_tasks(int max_N) {
+  const int np = h8_np_max(max_N), nch0 = (((np * kPanel + 8) >> 3) + 3) >> 2;
+  int n = 0;
+  for (int j = 0; j < np; j++) n += 2 * (nch0 - j) + 1;
+  return n + 4;
+}
+
+// staged coordinate stride: d rounded up to a compiled register width
+// (0 = generic rolled loop with stride d)
+static int h8_dm(int d) {
+#ifdef SBV_FORCE_DM0  // experiment: generic rolled generation loop
+  return 0;
+#endif
+  if (d <= 4) return 4;
+  if (d <= 8) return 8;
+  if (d <= 10) return 10;
+  if (d <= 12) return 12;
+  if (d <= 16) return 16;
+  return 0;
+}
+
+size_t h8_smem_bytes(int max_N, int d) {
+  const size_t Cp = (size_t)h8_np_max(max_N) * kPanel;
+  const size_t np = h8_np_max(max_N), nch = np + 1;
+  const size_t ints = 2 * np * nch + 2 * np + ((h8_max_tasks(max_N) + 1) & ~1);
+  const size_t ds = h8_dm(d) > 0 ? (size_t)h8_dm(d) : (size_t)d;
+  const size_t vs_smem = SBV_UPD_RING > 0 ? 0 : (size_t)max_N * ds;  // ring builds stage vs in global
+  return sizeof(double) * (4 * (size_t)kPanel * kDld + (kH8Threads / 32) * (size_t)kRingPerWarp +
+                           2 * SBV_MAX_D + (Cp + 8) + vs_smem) +
+         sizeof(int) * ((ints + 1) & ~(size_t)1);
+}
+
+// L panels of the largest block, then (ring builds) its staged coordinates
+static size_t h8_l_doubles(int max_N) {
+  const size_t Cp = (max_N + kPanel - 1) / kPanel * kPanel, R = Cp + 8, NP = Cp / kPanel;
+  size_t tot = 0;
+  for (size_t p = 0; p < NP; p++) tot += kPanel * (R - kPanel * p);
+  return (tot + 63) / 64 * 64;
+}
+
+size_t h8_ws_doubles(int max_N, int d) {
+  const size_t ds = h8_dm(d) > 0 ? (size_t)h8_dm(d) : (size_t)d;
+  const size_t vs = SBV_UPD_RING > 0 ? ((size_t)max_N * ds + 63) / 64 * 64 : 0;
+  return h8_l_doubles(max_N) + vs;
+}
+
+static H8Fn pick(double nu, int d) {
+  const int dm = h8_dm(d);
+  if (nu == 0.5) return h8_pick_nu1(dm);
+  if (nu == 1.5) return h8_pick_nu3(dm);
+  if (nu == 2.5) return h8_pick_nu5(dm);
+  return h8_pick_nu7(dm);
+}
+
+int h8_max_ctas_per_sm(size_t smem, int d) {
+  int best = 1 << 30;
+  for (double nu : {0.5, 1.5, 2.5, 3.5}) {  // the launch may use any smoothness
+    const H8Fn f = pick(nu, d);
+    int nb = 0;
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kH8Threads, smem);
+    best = nb < best ? nb : best;
+  }
+  return best;
+}
+
+cudaError_t launch_h8(const Ctx &c, const double *theta, cudaStream_t st) {
+  H8Args a;
+  a.Xp = c.Xperm;
+  a.yperm = c.yperm;
+  a.off = c.off;
+  a.nbr = c.nbr;
+  a.cnt = c.cnt;
+  a.local_blocks = c.local_blocks;
+  a.work_order = c.work_order;
+  a.k_local = c.k_local;
+  a.m = c.m > 0 ? c.m : 1;
+  a.d = c.d;
+  a.sigma2 = theta[0];
+  a.tau2 = theta[c.d + 2];
+  for (int j = 0; j < SBV_MAX_D; j++) a.inv_beta[j] = j < c.d ? 1.0 / theta[1 + j] : 0.0;
+  a.ws = c.ws;
+  a.ws_per_cta = c.ws_per_cta;
+  a.vs_off = h8_l_doubles(c.max_N);
+  a.queue = c.queue;
+  a.terms = c.terms;
+  a.quads = c.quads;
+  a.logdets = c.logdets;
+  a.status = c.status;
+  a.np_max = h8_np_max(c.max_N);
+  a.max_tasks = h8_max_tasks(c.max_N);
+  const double nu = theta[c.d + 1];
+  cudaError_t e = cudaMemsetAsync(c.queue, 0, sizeof(unsigned int), st);
+  if (e) return e;
+  if (c.k_local == 0) return cudaSuccess;
+  const int grid = c.h8_grid;
+  const size_t smem = c.h8_smem;
+  const H8Fn f = pick(nu, c.d);
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  f<<<grid, kH8Threads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace sbv

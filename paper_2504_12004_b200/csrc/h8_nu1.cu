@@ -1,0 +1,18 @@
+// h8_nu1.cu — k_h8 instantiations for 2 nu = 1 (one translation unit per
+// smoothness, so the variants compile in parallel).
+#include "h8_kernel.cuh"
+
+namespace sbv {
+
+H8Fn h8_pick_nu1(int dm) {
+  switch (dm) {
+    case 4: return k_h8<1, 4>;
+    case 8: return k_h8<1, 8>;
+    case 10: return k_h8<1, 10>;
+    case 12: return k_h8<1, 12>;
+    case 16: return k_h8<1, 16>;
+    default: return k_h8<1, 0>;
+  }
+}
+
+}  // namespace sbv

@@ -523,14 +523,15 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   if (h->max_N > 4096) return fail(h, SBV_ERR_UNSUPPORTED, "m + block size > 4096");
   if (h->h8_smem + 1024 > (size_t)smem_optin)
     return fail(h, SBV_ERR_UNSUPPORTED, "block + neighbour set too large for shared memory staging");
-  if (h->h8_smem != h->occ_smem) {  // occupancy query only when the smem size changes
+  if (h->h8_smem != h->occ_smem || d != h->occ_d) {  // occupancy query only on a change
     h->occ_smem = h->h8_smem;
-    h->occ_per_sm = h8_max_ctas_per_sm(h->h8_smem);
+    h->occ_d = d;
+    h->occ_per_sm = h8_max_ctas_per_sm(h->h8_smem, d);
   }
   int per_sm = h->occ_per_sm;
   if (per_sm < 1) per_sm = 1;
   h->h8_grid = (int)std::min<int64_t>((int64_t)sms * per_sm, std::max<int64_t>(h->k_local, 1));
-  h->ws_per_cta = h8_ws_doubles(std::max(h->max_N, 1));
+  h->ws_per_cta = h8_ws_doubles(std::max(h->max_N, 1), d);
   CU(ensure(h->ws, (size_t)h->h8_grid * h->ws_per_cta, unused));
   CU(cudaStreamSynchronize(st));
   tm.mark("meta");

@@ -70,6 +70,7 @@ struct Ctx {
   size_t h8_smem = 0;
   size_t occ_smem = 0;  // cached occupancy query
   int occ_per_sm = 0;
+  int occ_d = 0;
   std::unordered_map<void *, size_t> cap;  // device buffer capacities (bytes)
   // errors
   int64_t err_block = -1;
@@ -146,8 +147,8 @@ cudaError_t launch_knn(const double *Sperm, const int32_t *perm, const int64_t *
 cudaError_t launch_stage_eval(const double *y, const int32_t *perm, int64_t n, double *yperm,
                               cudaStream_t st);
 size_t h8_smem_bytes(int max_N, int d);
-size_t h8_ws_doubles(int max_N);
-int h8_max_ctas_per_sm(size_t smem);
+size_t h8_ws_doubles(int max_N, int d);
+int h8_max_ctas_per_sm(size_t smem, int d);
 cudaError_t launch_h8(const Ctx &c, const double *theta_host, cudaStream_t st);
 cudaError_t launch_reduce_chunks(const Ctx &c, cudaStream_t st);
 cudaError_t launch_final_reduce(const Ctx &c, cudaStream_t st);
