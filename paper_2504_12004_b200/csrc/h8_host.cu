@@ -31,7 +31,7 @@ size_t h8_smem_bytes(int max_N, int d) {
   const size_t np = h8_np_max(max_N), nch = np + 1;
   const size_t ints = 2 * np * nch + 2 * np + ((h8_max_tasks(max_N) + 1) & ~1);
   const size_t ds = h8_dm(d) > 0 ? (size_t)h8_dm(d) : (size_t)d;
-  const size_t vs_smem = SBV_UPD_RING > 0 ? 0 : (size_t)max_N * ds;  // ring builds stage vs in global
+  const size_t vs_smem = SBV_VS_GLOBAL ? 0 : (size_t)max_N * ds;  // else staged in global scratch
   return sizeof(double) * (4 * (size_t)kPanel * kDld + (kH8Threads / 32) * (size_t)kRingPerWarp +
                            2 * SBV_MAX_D + (Cp + 8) + vs_smem) +
          sizeof(int) * ((ints + 1) & ~(size_t)1);
@@ -47,7 +47,7 @@ static size_t h8_l_doubles(int max_N) {
 
 size_t h8_ws_doubles(int max_N, int d) {
   const size_t ds = h8_dm(d) > 0 ? (size_t)h8_dm(d) : (size_t)d;
-  const size_t vs = SBV_UPD_RING > 0 ? ((size_t)max_N * ds + 63) / 64 * 64 : 0;
+  const size_t vs = SBV_VS_GLOBAL ? ((size_t)max_N * ds + 63) / 64 * 64 : 0;
   return h8_l_doubles(max_N) + vs;
 }
 
