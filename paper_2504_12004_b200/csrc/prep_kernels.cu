@@ -84,17 +84,61 @@ cudaError_t select_anchors(int64_t n, int64_t k, uint64_t seed, int32_t *anchors
 }
 
 // Fast path: the keys are uniform 64-bit integers, so the k smallest lie below
-// T = (2k + 1024)/n * 2^64 with overwhelming probability.  Candidates below T
-// are appended, sorted by (key, index) with two small stable radix passes, and
-// the first k taken.  *bad is set when the candidate set cannot be trusted
-// (overflow, or fewer than k candidates); the caller then runs the full sort.
-__global__ void k_key_filter(int64_t n, uint64_t seed, uint64_t thr, int cap, uint64_t *ck, int32_t *ci,
-                             int *count) {
+// T = (2k + 1024)/n * 2^64 with overwhelming probability.  *bad is set when the
+// candidate set cannot be trusted (overflow of the 4k + 4096 slots, or fewer
+// than k candidates); the caller then runs the full sort.
+// Bucketed selection of the candidates below T: keys are uniform, so bucket
+// b = floor(key / w), w = T/B + 1, holds about (2k + 1024)/B of them and is
+// monotone in the key.  count -> exclusive scan -> scatter -> per-bucket
+// insertion sort; the candidate of global rank r < k is anchor r.
+// splitmix64 is a bijection of i (odd multiplier, xor-shifts, odd
+// multipliers), so keys never tie and the key alone orders them (Q9).
+constexpr int kScanThreads = 1024;
+constexpr int kMaxBuckets = kScanThreads * 256;
+
+__global__ void k_anc_count(int64_t n, uint64_t seed, uint64_t thr, uint64_t w, int *cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = splitmix64(seed, (uint64_t)i);
+    if (key < thr) atomicAdd(&cnt[key / w], 1);
+  }
+}
+
+// one CTA: start[b] = sum_{c<b} cnt[c]; cursor = start; start[B] = total
+__global__ void __launch_bounds__(kScanThreads) k_anc_scan(const int *cnt, int B, int *start, int *cursor,
+                                                           int *total) {
+  __shared__ int part[kScanThreads];
+  const int per = (B + kScanThreads - 1) / kScanThreads;
+  const int b0 = threadIdx.x * per, b1 = min(B, b0 + per);
+  int s = 0;
+  for (int b = b0; b < b1; b++) s += cnt[b];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 1; o < kScanThreads; o <<= 1) {  // Hillis-Steele inclusive scan
+    const int v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int run = threadIdx.x ? part[threadIdx.x - 1] : 0;
+  for (int b = b0; b < b1; b++) {
+    start[b] = run;
+    cursor[b] = run;
+    run += cnt[b];
+  }
+  if (threadIdx.x == kScanThreads - 1) {
+    start[B] = part[kScanThreads - 1];
+    *total = part[kScanThreads - 1];
+  }
+}
+
+__global__ void k_anc_scatter(int64_t n, uint64_t seed, uint64_t thr, uint64_t w, int cap, int *cursor,
+                              uint64_t *ck, int32_t *ci) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t key = splitmix64(seed, (uint64_t)i);
     if (key < thr) {
-      const int slot = atomicAdd(count, 1);
+      const int slot = atomicAdd(&cursor[key / w], 1);
       if (slot < cap) {
         ck[slot] = key;
         ci[slot] = (int32_t)i;
@@ -103,104 +147,58 @@ __global__ void k_key_filter(int64_t n, uint64_t seed, uint64_t thr, int cap, ui
   }
 }
 
-__global__ void k_fill_sentinel(int cap, uint64_t *ck, int32_t *ci) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x) {
-    ck[i] = UINT64_MAX;
-    ci[i] = INT32_MAX;
+__global__ void k_anc_finish(const int *start, int B, int cap, int64_t k, uint64_t *ck, int32_t *ci,
+                             int32_t *anchors) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int s = start[b], e = min(start[b + 1], cap);
+  if (s >= k || s >= e) return;
+  for (int x = s + 1; x < e; x++) {  // insertion sort by key (a handful of items)
+    const uint64_t kx = ck[x];
+    const int32_t ix = ci[x];
+    int y = x - 1;
+    while (y >= s && ck[y] > kx) {
+      ck[y + 1] = ck[y];
+      ci[y + 1] = ci[y];
+      y--;
+    }
+    ck[y + 1] = kx;
+    ci[y + 1] = ix;
   }
+  for (int r = s; r < e && r < k; r++) anchors[r] = ci[r];
 }
 
 __global__ void k_anchor_check(const int *count, int cap, int64_t k, int *bad) {
   if (threadIdx.x == 0 && blockIdx.x == 0) *bad = (*count > cap || *count < k) ? 1 : 0;
 }
 
-// Rank of each candidate in (key, index) order = number of candidates below
-// it; the candidate of rank r < k is anchor r.  splitmix64 is a bijection of
-// i (odd multiplier, xor-shifts, odd multipliers), so keys never tie and the
-// key alone orders them.  The candidate range is split over gridDim.y slices
-// whose partial ranks are summed with atomics.
-constexpr int kRankMaxCap = 4 * 16384 + 4096;
-constexpr int kRankSlices = 8;
-__global__ void __launch_bounds__(256) k_rank_candidates(const uint64_t *__restrict__ ck,
-                                                         const int *__restrict__ count, int cap,
-                                                         int *__restrict__ rank) {
-  __shared__ uint64_t sk[256];
-  const int c = min(*count, cap);
-  const int i = blockIdx.x * 256 + threadIdx.x;
-  if (blockIdx.x * 256 >= c) return;  // whole CTA beyond the candidates
-  const uint64_t key = i < c ? ck[i] : UINT64_MAX;
-  const int j0 = (int)((int64_t)c * blockIdx.y / gridDim.y), j1 = (int)((int64_t)c * (blockIdx.y + 1) / gridDim.y);
-  int r = 0;
-  for (int b = j0; b < j1; b += 256) {
-    __syncthreads();
-    const int j = b + threadIdx.x;
-    sk[threadIdx.x] = j < j1 ? ck[j] : UINT64_MAX;
-    __syncthreads();
-    const int lim = min(256, j1 - b);
-#pragma unroll 8
-    for (int x = 0; x < lim; x++) r += sk[x] < key ? 1 : 0;
-  }
-  if (i < c && r) atomicAdd(&rank[i], r);
-}
-
-__global__ void k_rank_scatter(const int32_t *__restrict__ ci, const int *__restrict__ count, int cap,
-                               const int *__restrict__ rank, int64_t k, int32_t *__restrict__ anchors) {
-  const int c = min(*count, cap);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x)
-    if (rank[i] < k) anchors[rank[i]] = ci[i];
-}
-
 cudaError_t select_anchors_fast(int64_t n, int64_t k, uint64_t seed, int32_t *anchors, int *bad,
                                 cudaStream_t st) {
   const double frac = std::min(1.0, (2.0 * k + 1024.0) / (double)n);
-  if (frac >= 0.25) {  // small n: nothing to gain, signal "use the full sort"
+  const int cap = (int)std::min<int64_t>(4 * k + 4096, INT32_MAX / 2);
+  int B = 1;
+  while (B < (2 * k + 1024) / 4) B <<= 1;
+  if (frac >= 0.25 || B > kMaxBuckets) {  // small n / huge k: signal "use the full sort"
     cudaMemsetAsync(bad, 0xff, sizeof(int), st);
     return cudaGetLastError();
   }
   const uint64_t thr = (uint64_t)(frac * 18446744073709551616.0);
-  const int cap = (int)(4 * k + 4096);
-  uint64_t *ck = nullptr, *ck2 = nullptr;
-  int32_t *ci = nullptr, *ci2 = nullptr;
-  int *count = nullptr;
-  void *tmp = nullptr;
-  size_t tb1 = 0, tb2 = 0;
+  const uint64_t w = thr / (uint64_t)B + 1;
+  char *buf = nullptr;
+  const size_t bytes = (size_t)cap * 12 + (size_t)(3 * B + 2) * 4 + 16;
   cudaError_t e;
-  if ((e = cudaMallocAsync(&ck, cap * 8, st))) return e;
-  if ((e = cudaMallocAsync(&ck2, cap * 8, st))) return e;
-  if ((e = cudaMallocAsync(&ci, cap * 4, st))) return e;
-  if ((e = cudaMallocAsync(&ci2, cap * 4, st))) return e;
-  if ((e = cudaMallocAsync(&count, sizeof(int), st))) return e;
-  cudaMemsetAsync(count, 0, sizeof(int), st);
-  if (cap > kRankMaxCap)  // the radix-sort path sorts all cap slots
-    k_fill_sentinel<<<std::max(1, std::min(cap / 256 + 1, 1024)), 256, 0, st>>>(cap, ck, ci);
-  k_key_filter<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(n, seed, thr, cap, ck,
-                                                                                  ci, count);
-  k_anchor_check<<<1, 32, 0, st>>>(count, cap, k, bad);
-  if (cap <= kRankMaxCap) {  // all-pairs rank: two launches instead of ~12 radix passes
-    int *rank = reinterpret_cast<int *>(ci2);
-    cudaMemsetAsync(rank, 0, cap * sizeof(int), st);
-    k_rank_candidates<<<dim3((cap + 255) / 256, kRankSlices), 256, 0, st>>>(ck, count, cap, rank);
-    k_rank_scatter<<<(cap + 255) / 256, 256, 0, st>>>(ci, count, cap, rank, k, anchors);
-    cudaFreeAsync(ck, st);
-    cudaFreeAsync(ck2, st);
-    cudaFreeAsync(ci, st);
-    cudaFreeAsync(ci2, st);
-    cudaFreeAsync(count, st);
-    return cudaGetLastError();
-  }
-  // (key, index) order: stable pass on the index, then a stable pass on the key
-  cub::DeviceRadixSort::SortPairs(nullptr, tb1, ci, ci2, ck, ck2, cap, 0, 32, st);
-  cub::DeviceRadixSort::SortPairs(nullptr, tb2, ck2, ck, ci2, ci, cap, 0, 64, st);
-  if ((e = cudaMallocAsync(&tmp, std::max(tb1, tb2), st))) return e;
-  cub::DeviceRadixSort::SortPairs(tmp, tb1, ci, ci2, ck, ck2, cap, 0, 32, st);
-  cub::DeviceRadixSort::SortPairs(tmp, tb2, ck2, ck, ci2, ci, cap, 0, 64, st);
-  cudaMemcpyAsync(anchors, ci, k * 4, cudaMemcpyDeviceToDevice, st);
-  cudaFreeAsync(tmp, st);
-  cudaFreeAsync(ck, st);
-  cudaFreeAsync(ck2, st);
-  cudaFreeAsync(ci, st);
-  cudaFreeAsync(ci2, st);
-  cudaFreeAsync(count, st);
+  if ((e = cudaMallocAsync(&buf, bytes, st))) return e;
+  uint64_t *ck = reinterpret_cast<uint64_t *>(buf);
+  int32_t *ci = reinterpret_cast<int32_t *>(ck + cap);
+  int *cnt = ci + cap, *start = cnt + B, *cursor = start + B + 1, *total = cursor + B;
+  cudaMemsetAsync(cnt, 0, (size_t)B * 4, st);
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  k_anc_count<<<grid, 256, 0, st>>>(n, seed, thr, w, cnt);
+  k_anc_scan<<<1, kScanThreads, 0, st>>>(cnt, B, start, cursor, total);
+  k_anchor_check<<<1, 32, 0, st>>>(total, cap, k, bad);
+  k_anc_scatter<<<grid, 256, 0, st>>>(n, seed, thr, w, cap, cursor, ck, ci);
+  k_anc_finish<<<(B + 255) / 256, 256, 0, st>>>(start, B, cap, k, ck, ci, anchors);
+  cudaFreeAsync(buf, st);
   return cudaGetLastError();
 }
 

@@ -318,6 +318,7 @@ void sbv_destroy(sbv_handle h) {
     if (h->ev[i]) cudaEventDestroy(h->ev[i]);
   if (h->result_host) cudaFreeHost(h->result_host);
   if (h->flag_host) cudaFreeHost(h->flag_host);
+  if (h->pin) cudaFreeHost(h->pin);
   delete h;
 }
 
@@ -372,16 +373,22 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   auto &unused = h->cap;
   Timer tm(h, 1);
 
-  CU(ensure(h->X, n * d, unused));
-  CU(cudaMemcpyAsync(h->X, X, n * d * sizeof(double), cudaMemcpyDefault, st));
+  // device inputs are read in place (valid for the duration of the call);
+  // host inputs are staged once
+  const double *Xd = X;
+  if (!is_device_ptr(X)) {
+    CU(ensure(h->X, n * d, unused));
+    CU(cudaMemcpyAsync(h->X, X, n * d * sizeof(double), cudaMemcpyDefault, st));
+    Xd = h->X;
+  }
   // finiteness flag: read back at the first host sync below (no extra stall)
   CU(ensure(h->flag, 2, unused));
   CU(cudaMemsetAsync(h->flag, 0, sizeof(int), st));
-  k_check_finite<<<grid_for(n * d), 256, 0, st>>>(h->X, n * d, h->flag);
+  k_check_finite<<<grid_for(n * d), 256, 0, st>>>(Xd, n * d, h->flag);
   CU(cudaMemcpyAsync(h->flag_host, h->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   tm.mark("h2d_X");
   CU(ensure(h->S, n * d, unused));
-  CU(launch_scale(h->X, n, d, scale, h->S, st));
+  CU(launch_scale(Xd, n, d, scale, h->S, st));
   tm.mark("H1_scale");
   CU(ensure(h->anchors, k, unused));
   if (h->use_grid) {  // filtered selection; verified at the next host sync (extents)
@@ -426,16 +433,28 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   tm.mark("H4_layout");
   // shard: 64-block chunks of zeta order dealt round-robin over ranks
   h->n_chunks = (k + kChunkBlocks - 1) / kChunkBlocks;
-  std::vector<int32_t> local(k / h->world + kChunkBlocks + 1);
+  // pinned host staging (async copies): local ids | off | cnt | LPT order
+  const int64_t loc_cap = k / h->world + kChunkBlocks + 1;
+  const size_t pin_bytes = sizeof(int64_t) * (size_t)(k + 1) + sizeof(int32_t) * (size_t)(3 * loc_cap + 2);
+  if (h->pin_cap < pin_bytes) {
+    if (h->pin) cudaFreeHost(h->pin);
+    h->pin = nullptr;
+    h->pin_cap = 0;
+    CU(cudaMallocHost(&h->pin, pin_bytes));
+    h->pin_cap = pin_bytes;
+  }
+  int64_t *off_h = reinterpret_cast<int64_t *>(h->pin);
+  int32_t *local = reinterpret_cast<int32_t *>(off_h + k + 1);
+  int32_t *cnt_h = local + loc_cap;
+  int32_t *order = cnt_h + loc_cap;
   {
     int64_t cnt_local = 0;
-    sbv_shard_blocks(k, h->rank, h->world, local.data(), &cnt_local);
-    local.resize(cnt_local);
+    sbv_shard_blocks(k, h->rank, h->world, local, &cnt_local);
+    h->k_local = cnt_local;
   }
-  h->k_local = (int64_t)local.size();
   h->n_chunks_local = (h->k_local + kChunkBlocks - 1) / kChunkBlocks;
   CU(ensure(h->local_blocks, h->k_local, unused));
-  CU(cudaMemcpyAsync(h->local_blocks, local.data(), h->k_local * sizeof(int32_t),
+  CU(cudaMemcpyAsync(h->local_blocks, local, h->k_local * sizeof(int32_t),
                      cudaMemcpyHostToDevice, st));
   CU(ensure(h->C, k * d, unused));
   CU(launch_centroids(h->Sperm, h->off, h->world > 1 ? h->local_blocks : nullptr, h->k_local, d,
@@ -459,11 +478,13 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   }
   tm.mark("H6_knn");
 
+  // block-major original inputs for H8 (queued before the host sync below)
+  CU(ensure(h->Xperm, n * d, unused));
+  CU(launch_gather_rows(Xd, h->perm, n, d, h->Xperm, st));
+
   // realised sizes -> LPT work order, statistics, H8 launch geometry
-  std::vector<int32_t> cnt_h(h->k_local);
-  std::vector<int64_t> off_h(k + 1);
-  CU(cudaMemcpyAsync(off_h.data(), h->off, (k + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  CU(cudaMemcpyAsync(cnt_h.data(), h->cnt, h->k_local * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(off_h, h->off, (k + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(cnt_h, h->cnt, h->k_local * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
   if (*h->flag_host) return fail(h, SBV_ERR_ARG, "X has non-finite entries");
   std::vector<int32_t> Nt(h->k_local);
@@ -489,7 +510,6 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   for (int64_t li = 0; li < h->k_local; li++)
     h->h8_bytes += (double)Nt[li] * (d + 1) * 8.0 + (double)cnt_h[li] * 4.0 + 4 * 8.0;
   // LPT order (N_t descending, ties by local index): a stable counting sort
-  std::vector<int32_t> order(h->k_local);
   {
     std::vector<int64_t> bucket((size_t)h->max_N + 2, 0);
     for (int64_t li = 0; li < h->k_local; li++) bucket[h->max_N - Nt[li] + 1]++;
@@ -497,12 +517,10 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
     for (int64_t li = 0; li < h->k_local; li++) order[bucket[h->max_N - Nt[li]]++] = (int32_t)li;
   }
   CU(ensure(h->work_order, h->k_local, unused));
-  CU(cudaMemcpyAsync(h->work_order, order.data(), h->k_local * sizeof(int32_t),
+  CU(cudaMemcpyAsync(h->work_order, order, h->k_local * sizeof(int32_t),
                      cudaMemcpyHostToDevice, st));
 
   // per-eval buffers
-  CU(ensure(h->Xperm, n * d, unused));
-  CU(launch_gather_rows(h->X, h->perm, n, d, h->Xperm, st));
   CU(ensure(h->yperm, n, unused));
   CU(ensure(h->ybuf, n, unused));
   CU(ensure(h->terms, h->k_local, unused));

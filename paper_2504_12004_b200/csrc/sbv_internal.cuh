@@ -63,6 +63,8 @@ struct Ctx {
   int use_grid = 1;                               // SBV_GRID=0 forces the brute-force kernels
   int *flag = nullptr;            // device: non-finite input flag
   int *flag_host = nullptr;       // pinned mirror
+  char *pin = nullptr;            // pinned staging of prepare's host-side tables
+  size_t pin_cap = 0;
   unsigned int *queue = nullptr;  // work counter
   double *ws = nullptr;           // H8 per-CTA L workspaces
   size_t ws_per_cta = 0;
