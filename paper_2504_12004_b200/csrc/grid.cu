@@ -365,21 +365,103 @@ __global__ void __launch_bounds__(256) k_rac_grid(const double *__restrict__ S, 
   block_of[i - i0] = arg;
 }
 
-cudaError_t launch_rac_grid(const double *S, int64_t n, int64_t i0, int d, const int32_t *anchors, const GridDesc &g,
-                            const int32_t *a_start, const int32_t *a_list, int32_t *block_of,
-                            cudaStream_t st) {
+// Anchor rows gathered in cell order (AC) with their ranks, so a cell's
+// candidates are consecutive rows: no indirection through `anchors`.
+__global__ void k_gather_anchor_rows(const double *__restrict__ S, const int32_t *__restrict__ anchors,
+                                     const int32_t *__restrict__ a_list, int64_t k, int d,
+                                     double *__restrict__ AC, int32_t *__restrict__ arank) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < k * d;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / d;
+    const int j = (int)(e - r * d);
+    const int32_t rank = a_list[r];
+    AC[e] = S[(int64_t)anchors[rank] * d + j];
+    if (j == 0) arank[r] = rank;
+  }
+}
+
+// Points are visited in anchor-grid cell order (`order`, relative to i0), so
+// the lanes of a warp search the same cells and read the same anchor rows.
+template <int DM>
+__global__ void __launch_bounds__(256) k_rac_grid2(const double *__restrict__ S, const int32_t *__restrict__ order,
+                                                   int64_t count, int64_t i0, int d,
+                                                   const double *__restrict__ AC,
+                                                   const int32_t *__restrict__ arank, GridDesc g,
+                                                   const int32_t *__restrict__ a_start,
+                                                   int32_t *__restrict__ block_of) {
+  const int64_t tt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (tt >= count) return;
+  const int64_t il = order[tt], i = i0 + il;
+  double p[DM];
+#pragma unroll
+  for (int j = 0; j < DM; j++) p[j] = j < d ? S[i * d + j] : 0.0;
+  RingQ q;
+  for (int x = 0; x < 3; x++) {
+    q.x[x] = x < g.G ? S[i * d + g.dim[x]] : 0.0;
+    q.cq[x] = x < g.G ? cell_coord(q.x[x], g.lo[x], g.h[x], g.nc[x]) : 0;
+  }
+  double best = INFINITY;
+  int32_t arg = INT32_MAX;
+  for (int r = 0;; r++) {
+    for_ring(g, q, r, [&](int cell, double lb2) {
+      if (!may_hold(lb2, best)) return;
+      for (int e = a_start[cell]; e < a_start[cell + 1]; e++) {
+        const int32_t rank = arank[e];
+        const double *s = AC + (int64_t)e * d;
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < DM; j++)
+          if (j < d) {
+            const double t = p[j] - s[j];
+            acc = __fma_rn(t, t, acc);
+          }
+        if (acc < best || (acc == best && rank < arg)) {  // Alg.3 argmin, ties -> lowest rank
+          best = acc;
+          arg = rank;
+        }
+      }
+    });
+    const double lb = ring_lb2(g, q, r);
+    if (lb < 0.0) break;
+    if (arg != INT32_MAX && !may_hold(lb, best)) break;
+  }
+  block_of[il] = arg;
+}
+
+cudaError_t launch_rac_grid(const double *S, int64_t n, int64_t i0, int d, const int32_t *anchors, int64_t k,
+                            const GridDesc &g, const int32_t *a_start, const int32_t *a_list,
+                            int32_t *block_of, cudaStream_t st) {
   if (n <= i0) return cudaSuccess;
-  const int grid = (int)((n - i0 + 255) / 256);
+  const int64_t count = n - i0;
+  // scratch: anchor rows in cell order + ranks, the slice's points sorted by cell
+  double *AC = nullptr;
+  int32_t *arank = nullptr, *order = nullptr, *pstart = nullptr;
+  cudaError_t e;
+  if ((e = cudaMallocAsync(&AC, sizeof(double) * k * d, st))) return e;
+  if ((e = cudaMallocAsync(&arank, sizeof(int32_t) * k, st))) return e;
+  if ((e = cudaMallocAsync(&order, sizeof(int32_t) * count, st))) return e;
+  if ((e = cudaMallocAsync(&pstart, sizeof(int32_t) * (g.ncells + 1), st))) return e;
+  k_gather_anchor_rows<<<(int)std::max<int64_t>(1, std::min<int64_t>((k * d + 255) / 256, 148 * 16)), 256, 0, st>>>(
+      S, anchors, a_list, k, d, AC, arank);
+  if ((e = build_cells(S + i0 * d, nullptr, count, d, g, pstart, order, st))) return e;
+  const int grid = (int)((count + 255) / 256);
+#define SBV_RAC(DMv) \
+  k_rac_grid2<DMv><<<grid, 256, 0, st>>>(S, order, count, i0, d, AC, arank, g, a_start, block_of)
   if (d <= 4)
-    k_rac_grid<4><<<grid, 256, 0, st>>>(S, n, i0, d, anchors, g, a_start, a_list, block_of);
+    SBV_RAC(4);
   else if (d <= 8)
-    k_rac_grid<8><<<grid, 256, 0, st>>>(S, n, i0, d, anchors, g, a_start, a_list, block_of);
+    SBV_RAC(8);
   else if (d <= 16)
-    k_rac_grid<16><<<grid, 256, 0, st>>>(S, n, i0, d, anchors, g, a_start, a_list, block_of);
+    SBV_RAC(16);
   else if (d <= 32)
-    k_rac_grid<32><<<grid, 256, 0, st>>>(S, n, i0, d, anchors, g, a_start, a_list, block_of);
+    SBV_RAC(32);
   else
-    k_rac_grid<64><<<grid, 256, 0, st>>>(S, n, i0, d, anchors, g, a_start, a_list, block_of);
+    SBV_RAC(64);
+#undef SBV_RAC
+  cudaFreeAsync(AC, st);
+  cudaFreeAsync(arank, st);
+  cudaFreeAsync(order, st);
+  cudaFreeAsync(pstart, st);
   return cudaGetLastError();
 }
 

@@ -414,11 +414,11 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
       const int64_t chunk = (n + h->world - 1) / h->world;
       CU(ensure(h->block_of, chunk * h->world, unused));
       const int64_t i0 = std::min<int64_t>(n, h->rank * chunk), i1 = std::min<int64_t>(n, i0 + chunk);
-      CU(launch_rac_grid(h->S, i1, i0, d, h->anchors, ga, h->a_start, h->a_list,
+      CU(launch_rac_grid(h->S, i1, i0, d, h->anchors, k, ga, h->a_start, h->a_list,
                          h->block_of + h->rank * chunk, st));
       NC(ncclAllGather(h->block_of + h->rank * chunk, h->block_of, (size_t)chunk, ncclInt32, h->comm, st));
     } else {
-      CU(launch_rac_grid(h->S, n, 0, d, h->anchors, ga, h->a_start, h->a_list, h->block_of, st));
+      CU(launch_rac_grid(h->S, n, 0, d, h->anchors, k, ga, h->a_start, h->a_list, h->block_of, st));
     }
     CU(anchor_own_block(h->anchors, k, h->block_of, st));
   } else {

@@ -115,9 +115,9 @@ cudaError_t data_extents(const double *S, int64_t n, int d, double *lo_hi_host, 
 GridDesc make_grid(const double *lo_hi, int d, int64_t count, double per_cell);
 cudaError_t build_cells(const double *S, const int32_t *rows, int64_t count, int d, const GridDesc &g,
                         int32_t *start, int32_t *list, cudaStream_t st);
-cudaError_t launch_rac_grid(const double *S, int64_t n, int64_t i0, int d, const int32_t *anchors, const GridDesc &g,
-                            const int32_t *a_start, const int32_t *a_list, int32_t *block_of,
-                            cudaStream_t st);
+cudaError_t launch_rac_grid(const double *S, int64_t n, int64_t i0, int d, const int32_t *anchors, int64_t k,
+                            const GridDesc &g, const int32_t *a_start, const int32_t *a_list,
+                            int32_t *block_of, cudaStream_t st);
 cudaError_t launch_knn_grid(const double *Sperm, const int32_t *perm, const int64_t *off,
                             const double *C, const int32_t *local_blocks, int64_t k_local, int d,
                             int m, const KnnLevels &lv, const int32_t *c_start, const int32_t *c_list,
