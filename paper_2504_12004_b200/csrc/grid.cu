@@ -320,51 +320,6 @@ __device__ __forceinline__ void for_ring(const GridDesc &g, const RingQ &q, int 
 }
 
 // ------------------------------------------------------------------ H3 RAC
-template <int DM>
-__global__ void __launch_bounds__(256) k_rac_grid(const double *__restrict__ S, int64_t n, int64_t i0, int d,
-                                                  const int32_t *__restrict__ anchors, GridDesc g,
-                                                  const int32_t *__restrict__ a_start,
-                                                  const int32_t *__restrict__ a_list,
-                                                  int32_t *__restrict__ block_of) {
-  // points [i0, n); block_of is indexed relative to i0 (one rank's slice)
-  const int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double p[DM];
-#pragma unroll
-  for (int j = 0; j < DM; j++) p[j] = j < d ? S[i * d + j] : 0.0;
-  RingQ q;
-  for (int x = 0; x < 3; x++) {
-    q.x[x] = x < g.G ? S[i * d + g.dim[x]] : 0.0;
-    q.cq[x] = x < g.G ? cell_coord(q.x[x], g.lo[x], g.h[x], g.nc[x]) : 0;
-  }
-  double best = INFINITY;
-  int32_t arg = INT32_MAX;
-  for (int r = 0;; r++) {
-    for_ring(g, q, r, [&](int cell, double lb2) {
-      if (!may_hold(lb2, best)) return;
-      for (int e = a_start[cell]; e < a_start[cell + 1]; e++) {
-        const int32_t rank = a_list[e];
-        const double *s = S + (int64_t)anchors[rank] * d;
-        double acc = 0.0;
-#pragma unroll
-        for (int j = 0; j < DM; j++)
-          if (j < d) {
-            const double t = p[j] - s[j];
-            acc = __fma_rn(t, t, acc);
-          }
-        if (acc < best || (acc == best && rank < arg)) {  // Alg.3 argmin, ties -> lowest rank
-          best = acc;
-          arg = rank;
-        }
-      }
-    });
-    const double lb = ring_lb2(g, q, r);
-    if (lb < 0.0) break;
-    if (arg != INT32_MAX && !may_hold(lb, best)) break;
-  }
-  block_of[i - i0] = arg;
-}
-
 // Anchor rows gathered in cell order (AC) with their ranks, so a cell's
 // candidates are consecutive rows: no indirection through `anchors`.
 __global__ void k_gather_anchor_rows(const double *__restrict__ S, const int32_t *__restrict__ anchors,
@@ -471,7 +426,16 @@ cudaError_t launch_rac_grid(const double *S, int64_t n, int64_t i0, int d, const
 // admissible ones are a prefix).  Keys (dist2, original index) below the
 // current m-th best are appended to a per-warp shared-memory buffer that is
 // bitonic-sorted and cut to m whenever it fills.
-constexpr int kKnnWarps = 4;
+#ifndef SBV_KNN_WCAP
+#define SBV_KNN_WCAP 512  // per-warp candidate buffer (16 B entries): occupancy vs compactions
+#endif
+#ifndef SBV_KNN_MINCAP
+#define SBV_KNN_MINCAP(m) ((m) + 192)  // headroom between compactions (cfg2: 512 entries, 1.2 -> 1.0 ms)
+#endif
+#ifndef SBV_KNN_WARPS
+#define SBV_KNN_WARPS 4
+#endif
+constexpr int kKnnWarps = SBV_KNN_WARPS;
 constexpr int kKnnWcap = 1024;
 
 struct WCand {
@@ -699,8 +663,8 @@ cudaError_t launch_knn_grid(const double *Sperm, const int32_t *perm, const int6
   const int thr = 32 * kKnnWarps;
   // per-warp candidate buffer: the smallest power of two >= m + 160 (headroom
   // between compactions) keeps shared memory low and occupancy high
-  int wcap = 1024;  // measured: 512 at m=200 costs more compactions than it gains
-  while (wcap < 2 * m + 128) wcap <<= 1;
+  int wcap = SBV_KNN_WCAP;  // measured at cfg2: 256 / 512 / 1024 / 2048 -> 1.23 / 1.00 / 1.20 / 2.38 ms
+  while (wcap < SBV_KNN_MINCAP(m)) wcap <<= 1;
   const int smem = (int)(sizeof(WCand) * kKnnWarps * wcap);
 #define SBV_KNN(DMv)                                                                                    \
   do {                                                                                                  \
