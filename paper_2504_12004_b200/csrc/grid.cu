@@ -432,6 +432,9 @@ cudaError_t launch_rac_grid(const double *S, int64_t n, int64_t i0, int d, const
 #ifndef SBV_KNN_MINCAP
 #define SBV_KNN_MINCAP(m) ((m) + 192)  // headroom between compactions (cfg2: 512 entries, 1.2 -> 1.0 ms)
 #endif
+#ifndef SBV_KNN_SLACK
+#define SBV_KNN_SLACK 0  // ring-end compaction once the buffer holds more than m + slack
+#endif
 #ifndef SBV_KNN_WARPS
 #define SBV_KNN_WARPS 4
 #endif
@@ -474,6 +477,86 @@ __device__ void warp_bitonic(WCand *buf, int cnt, int lane) {
   }
 }
 
+// Warp radix select: the m-th smallest key (d2, orig) among buf[0, cnt)
+// (1 <= m <= cnt).  d2 >= 0, so its IEEE bits order like the values; eight
+// 8-bit passes over d2 with a per-warp 256-bin shared histogram, then (only
+// when several entries share that d2) four passes over orig.  ~1k
+// instructions per call instead of a 512-entry bitonic sort.
+__device__ __forceinline__ int hist_find(unsigned *hist, int lane, int &k) {
+  // hist holds 256 counts; return the digit whose cumulative range holds the
+  // k-th (1-based) item, and reduce k by the items in smaller digits
+  unsigned c[8], s = 0;
+#pragma unroll
+  for (int x = 0; x < 8; x++) {
+    c[x] = hist[lane * 8 + x];
+    s += c[x];
+  }
+  unsigned incl = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const unsigned excl = incl - s;
+  int digit = -1, below = 0;
+  if ((unsigned)k > excl && (unsigned)k <= incl) {
+    unsigned run = excl;
+#pragma unroll
+    for (int x = 0; x < 8; x++) {
+      if (digit < 0 && (unsigned)k <= run + c[x]) {
+        digit = lane * 8 + x;
+        below = (int)run;
+      }
+      run += c[x];
+    }
+  }
+  const unsigned owner = __ballot_sync(0xffffffffu, digit >= 0);
+  const int src = __ffs(owner) - 1;
+  digit = __shfl_sync(0xffffffffu, digit, src);
+  below = __shfl_sync(0xffffffffu, below, src);
+  k -= below;
+  return digit;
+}
+
+__device__ void warp_select(const WCand *buf, int cnt, int m, int lane, unsigned *hist, double &thr_d,
+                            int32_t &thr_i) {
+  unsigned long long prefix = 0, pmask = 0;
+  int k = m;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+#pragma unroll
+    for (int x = 0; x < 8; x++) hist[lane * 8 + x] = 0;
+    __syncwarp();
+    for (int i = lane; i < cnt; i += 32) {
+      const unsigned long long u = (unsigned long long)__double_as_longlong(buf[i].d2);
+      if ((u & pmask) == prefix) atomicAdd(&hist[(u >> shift) & 255], 1u);
+    }
+    __syncwarp();
+    const int digit = hist_find(hist, lane, k);
+    __syncwarp();
+    prefix |= (unsigned long long)digit << shift;
+    pmask |= 255ull << shift;
+  }
+  thr_d = __longlong_as_double((long long)prefix);
+  // k-th smallest orig among the entries whose d2 equals thr_d
+  unsigned pre = 0, pm = 0;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+#pragma unroll
+    for (int x = 0; x < 8; x++) hist[lane * 8 + x] = 0;
+    __syncwarp();
+    for (int i = lane; i < cnt; i += 32) {
+      const WCand e = buf[i];
+      const unsigned o = (unsigned)e.orig;
+      if (e.d2 == thr_d && (o & pm) == pre) atomicAdd(&hist[(o >> shift) & 255], 1u);
+    }
+    __syncwarp();
+    const int digit = hist_find(hist, lane, k);
+    __syncwarp();
+    pre |= (unsigned)digit << shift;
+    pm |= 255u << shift;
+  }
+  thr_i = (int32_t)pre;
+}
+
 template <int DM>
 __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
     const double *__restrict__ Sperm, const int32_t *__restrict__ perm,
@@ -481,7 +564,8 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
     const int32_t *__restrict__ local_blocks, int64_t k_local, int d, int m, KnnLevels lv,
     const int32_t *__restrict__ c_start_all, const int32_t *__restrict__ c_list, int32_t *__restrict__ nbr,
     int32_t *__restrict__ cnt_out, int wcap) {
-  extern __shared__ WCand sbuf[];  // kKnnWarps x wcap
+  extern __shared__ WCand sbuf[];  // kKnnWarps x wcap, then kKnnWarps x 256 histogram bins
+  unsigned *hist = reinterpret_cast<unsigned *>(sbuf + kKnnWarps * wcap) + (threadIdx.x >> 5) * 256;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t li = blockIdx.x * (int64_t)kKnnWarps + w;
   if (li >= k_local) return;
@@ -510,13 +594,29 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
   double thr_d = INFINITY;
   int32_t thr_i = INT32_MAX;
   int seen = 0;  // admissible points seen (for the "fewer than m exist" exit)
+  // keep the m smallest keys (unsorted) and set the threshold to the m-th
   auto compact = [&]() {
     __syncwarp();
-    warp_bitonic(buf, count, lane);
-    count = min(count, m);
-    if (count == m) {
-      thr_d = buf[m - 1].d2;
-      thr_i = buf[m - 1].orig;
+    if (count > m) {
+      warp_select(buf, count, m, lane, hist, thr_d, thr_i);
+      int kept = 0;
+      for (int base = 0; base < count; base += 32) {
+        const int i = base + lane;
+        WCand e;
+        bool keep = false;
+        if (i < count) {
+          e = buf[i];
+          keep = !wless(thr_d, thr_i, e.d2, e.orig);  // e <= threshold
+        }
+        const unsigned mk = __ballot_sync(0xffffffffu, keep);
+        __syncwarp();  // every lane has read its entry before the chunk is overwritten
+        if (keep) buf[kept + __popc(mk & ((1u << lane) - 1))] = e;
+        kept += __popc(mk);
+        __syncwarp();
+      }
+      count = kept;  // == m (keys are unique)
+    } else if (count == m && thr_d == INFINITY) {
+      warp_select(buf, count, m, lane, hist, thr_d, thr_i);  // the m-th = the largest
     }
     __syncwarp();
   };
@@ -641,12 +741,13 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
         // a full sort only when the threshold is unset or the buffer has
         // grown well past m; otherwise test termination against the current
         // (conservative) m-th best
-        if (thr_d == INFINITY || count > m + 128) compact();
+        if (thr_d == INFINITY || count > m + SBV_KNN_SLACK) compact();
         if (!may_hold(lb, thr_d)) break;
       }
     }
   }
   compact();
+  warp_bitonic(buf, count, lane);  // the final m (or fewer) in (d2, orig) order
   const int keep = min(count, min(m, A));
   for (int j = lane; j < m; j += 32) nbr[li * m + j] = j < keep ? buf[j].pos : -1;
   if (lane == 0) cnt_out[li] = keep;
@@ -665,7 +766,7 @@ cudaError_t launch_knn_grid(const double *Sperm, const int32_t *perm, const int6
   // between compactions) keeps shared memory low and occupancy high
   int wcap = SBV_KNN_WCAP;  // measured at cfg2: 256 / 512 / 1024 / 2048 -> 1.23 / 1.00 / 1.20 / 2.38 ms
   while (wcap < SBV_KNN_MINCAP(m)) wcap <<= 1;
-  const int smem = (int)(sizeof(WCand) * kKnnWarps * wcap);
+  const int smem = (int)(sizeof(WCand) * kKnnWarps * wcap + sizeof(unsigned) * kKnnWarps * 256);
 #define SBV_KNN(DMv)                                                                                    \
   do {                                                                                                  \
     cudaFuncSetAttribute(k_knn_grid<DMv>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);          \
