@@ -74,6 +74,13 @@ def lib():
                                         _p, _p, _p, _p]
         L.orc_block_term_at.restype = ctypes.c_int
         L.orc_max_threads.restype = ctypes.c_int
+        L.orc_knn_pred.argtypes = [_p, _i64, _i32, _p, _i32, _p]
+        L.orc_knn_pred.restype = _i32
+        L.orc_predict_block.argtypes = [_p, _p, _p, _i32, _p, _i32, _p, _i32, _p, _p, _p]
+        L.orc_predict_block.restype = ctypes.c_int
+        L.orc_simulate.argtypes = [_p, _p, _i64, _i32, _u64, _dbl, _p, _p, _p, _p]
+        L.orc_z_crit.argtypes = [_dbl]
+        L.orc_z_crit.restype = _dbl
         _lib = L
     return _lib
 
@@ -273,3 +280,68 @@ def prepare(X, bs: int, m: int, scale_, seed: int, nthreads: int = 0):
     C = centroids(S, perm, off)
     nbr, cnt = knn(S, perm, off, C, m, nthreads)
     return dict(S=S, k=k, anchors=anc, block_of=bo, perm=perm, off=off, C=C, nbr=nbr, cnt=cnt)
+
+
+# ----------------------------------------------------------------- O10-O12 (NEXT N2)
+def knn_pred(S, c, m: int):
+    """Prediction-mode m-NN of centroid c over ALL training rows of S (original indices)."""
+    S, ps = _c(S, np.float64)
+    c, pc = _c(c, np.float64)
+    out = np.empty(max(m, 1), dtype=np.int32)
+    k = lib().orc_knn_pred(ps, S.shape[0], S.shape[1], pc, m, out.ctypes.data_as(_p))
+    return out[:k].copy()
+
+
+def predict_block(Xtr, y, Xte, J, B, theta):
+    """One test block: (mean, var) of Sec.4.1 restricted to NN(B*)."""
+    Xtr, px = _c(Xtr, np.float64)
+    y, py = _c(y, np.float64)
+    Xte, pt = _c(Xte, np.float64)
+    J, pj = _c(np.asarray(J, dtype=np.int32).reshape(-1), np.int32)
+    B, pb = _c(np.asarray(B, dtype=np.int32).reshape(-1), np.int32)
+    th, pth = _c(theta, np.float64)
+    mean = np.empty(B.shape[0])
+    var = np.empty(B.shape[0])
+    rc = lib().orc_predict_block(px, py, pt, Xtr.shape[1], pj, J.shape[0], pb, B.shape[0], pth,
+                                 mean.ctypes.data_as(_p), var.ctypes.data_as(_p))
+    if rc != 0:
+        raise NotPD(-1, 1)
+    return mean, var
+
+
+def predict(Xtr, y, Xte, bs_pred: int, m_pred: int, scale_, theta, seed: int = 3):
+    """Eq.3 prediction: test blocks by the same anchors + RAC (O2-O5) on the
+    scaled test inputs, prediction-mode NN over the training set, per-block
+    conditional mean / variance.  Returns (mean, var, blocks) in test order."""
+    S = scale(Xtr, scale_)
+    St = scale(Xte, scale_)
+    nt = Xte.shape[0]
+    k = num_blocks(nt, bs_pred)
+    anc = anchors(nt, k, seed)
+    bo = rac(St, anc)
+    perm, off = layout(bo, k)
+    C = centroids(St, perm, off)
+    mean = np.empty(nt)
+    var = np.empty(nt)
+    nbrs = []
+    for t in range(k):
+        J = knn_pred(S, C[t], m_pred)
+        B = perm[off[t]:off[t + 1]]
+        mu, v = predict_block(Xtr, y, Xte, J, B, theta)
+        mean[B] = mu
+        var[B] = v
+        nbrs.append(J)
+    return mean, var, dict(anchors=anc, block_of=bo, perm=perm, off=off, C=C, nbr=nbrs)
+
+
+def z_crit(ci_level: float) -> float:
+    return float(lib().orc_z_crit(ci_level))
+
+
+def simulate(mean, var, n_sim: int, seed: int, ci_level: float = 0.95):
+    mean, pm = _c(mean, np.float64)
+    var, pv = _c(var, np.float64)
+    n = mean.shape[0]
+    out = [np.empty(n) for _ in range(4)]
+    lib().orc_simulate(pm, pv, n, n_sim, seed, z_crit(ci_level), *[o.ctypes.data_as(_p) for o in out])
+    return tuple(out)

@@ -25,6 +25,14 @@
  *                       with the -(bs/2) log 2pi constant of Eq.1 (Q2)
  *   O9 orc_loglik       Alg.1 Step 4-5: sum of block terms in zeta order
  *                       (Neumaier-compensated, Q15)
+ *  NEXT row N2, prediction:
+ *   O10 orc_knn_pred    Eq.3 NN(B*_j) "selected from the y": exact m-NN
+ *                       of the test-block centroid over ALL training points
+ *   O11 orc_predict_block  Sec.4.1 restricted to NN(B*_j):
+ *                       mu = Sigma_{*J} Sigma_JJ^-1 y_J, var = diag(Sigma_** - Sigma_{*J}
+ *                       Sigma_JJ^-1 Sigma_{J*}); Sec.5.5
+ *   O12 orc_simulate    Sec.5.5: n_sim draws N(mu_j, var_j) per point,
+ *                       sample mean / sd / (1 - alpha) interval
  *
  * Pins (tests/test_oracle_*.py) tie every function to something other than
  * itself: splitmix64 published vectors, scipy.special.kv Matern, dense Eq.1
@@ -462,4 +470,132 @@ int orc_max_threads(void) {
 #else
   return 1;
 #endif
+}
+
+/* ------------------------------------------------------------------ O10 */
+/* Prediction-mode NN (Eq.3): every training point is a
+ * candidate (no ordering constraint); full sort by (dist2(c, s), index), first
+ * min(m, n) kept.  S: n x d scaled training inputs; c: the test-block
+ * centroid in the same scaled space.  Returns the count. */
+int32_t orc_knn_pred(const double *S, int64_t n, int32_t d, const double *c, int32_t m,
+                     int32_t *nbr) {
+  int32_t cnt = (int32_t)(n < m ? n : m);
+  for (int32_t j = 0; j < m; j++) nbr[j] = -1;
+  orc_cand *cd = (orc_cand *)malloc(sizeof(orc_cand) * (n > 0 ? n : 1));
+  for (int64_t p = 0; p < n; p++) {
+    cd[p].idx = p;
+    cd[p].d2 = orc_dist2(c, S + p * d, d);
+  }
+  qsort(cd, n, sizeof(orc_cand), cmp_cand);
+  for (int32_t j = 0; j < cnt; j++) nbr[j] = (int32_t)cd[j].idx;
+  free(cd);
+  return cnt;
+}
+
+/* ------------------------------------------------------------------ O11 */
+/* One test block's conditional distribution (Sec.4.1 P:176-183 with the
+ * training set replaced by NN(B*_j), Eq.3): Xtr/y training inputs (original
+ * scale) and observations, J[0..mt) training indices, Xte test inputs,
+ * B[0..bst) test indices.  Written out with explicit matrices:
+ *   L = POTRF(Sigma_JJ); alpha = L^-T L^-1 y_J; mean = Sigma_{*J} alpha;
+ *   V = L^-1 Sigma_{J*}; var_i = Sigma_{**,ii} - sum_q V_{qi}^2.
+ * Sigma_{**} carries the nugget on its diagonal (Q3): var is the predictive
+ * variance of y*.  Returns ORC_ERR_NOT_PD if Sigma_JJ is not positive definite. */
+int orc_predict_block(const double *Xtr, const double *y, const double *Xte, int32_t d,
+                      const int32_t *J, int32_t mt, const int32_t *B, int32_t bst,
+                      const double *theta, double *mean, double *var) {
+  int64_t m = mt, b = bst;
+  double *Sjj = (double *)malloc(sizeof(double) * (m > 0 ? m * m : 1));
+  double *Sjb = (double *)malloc(sizeof(double) * (m > 0 ? m * b : 1));
+  double *a = (double *)malloc(sizeof(double) * (m > 0 ? m : 1));
+  double *col = (double *)malloc(sizeof(double) * (m > 0 ? m : 1));
+  int rc = ORC_OK;
+  for (int64_t i = 0; i < m; i++)
+    for (int64_t j = 0; j < m; j++)
+      Sjj[i * m + j] = orc_kernel(Xtr + (int64_t)J[i] * d, Xtr + (int64_t)J[j] * d, d, theta, i == j);
+  for (int64_t i = 0; i < m; i++)
+    for (int64_t j = 0; j < b; j++)
+      Sjb[i * b + j] = orc_kernel(Xtr + (int64_t)J[i] * d, Xte + (int64_t)B[j] * d, d, theta, 0);
+  for (int64_t j = 0; j < b; j++) {
+    mean[j] = 0.0;
+    var[j] = orc_kernel(Xte + (int64_t)B[j] * d, Xte + (int64_t)B[j] * d, d, theta, 1);
+  }
+  if (m > 0) {
+    if (chol_lower(Sjj, m) != 0) {
+      rc = ORC_ERR_NOT_PD;
+      goto done;
+    }
+    for (int64_t i = 0; i < m; i++) a[i] = y[J[i]];
+    forward_subst(Sjj, m, a); /* L^-1 y_J */
+    for (int64_t i = m - 1; i >= 0; i--) { /* L^-T (L^-1 y_J) */
+      double s = a[i];
+      for (int64_t q = i + 1; q < m; q++) s = s - Sjj[q * m + i] * a[q];
+      a[i] = s / Sjj[i * m + i];
+    }
+    for (int64_t j = 0; j < b; j++) {
+      double s = 0.0;
+      for (int64_t i = 0; i < m; i++) s = s + Sjb[i * b + j] * a[i];
+      mean[j] = s;
+      for (int64_t i = 0; i < m; i++) col[i] = Sjb[i * b + j];
+      forward_subst(Sjj, m, col); /* V_{.j} = L^-1 Sigma_{J j} */
+      double v = 0.0;
+      for (int64_t i = 0; i < m; i++) v = v + col[i] * col[i];
+      var[j] = var[j] - v;
+    }
+  }
+done:
+  free(Sjj);
+  free(Sjb);
+  free(a);
+  free(col);
+  return rc;
+}
+
+/* ------------------------------------------------------------------ O12 */
+/* Sec.5.5: for point j, n_sim draws
+ *   x_{j,s} = mean_j + sqrt(var_j) * z_{j,s},
+ * z from a counter-based generator both sides implement: u1, u2 =
+ * (splitmix64(seed, 2c) >> 11 + 0.5) 2^-53, (splitmix64(seed, 2c + 1) >> 11 + 0.5) 2^-53
+ * with c = j n_sim + s, and Box-Muller z = sqrt(-2 ln u1) cos(2 pi u2).
+ * Outputs the sample mean, the sample sd (divisor n_sim - 1) and mu~ -/+ z_crit sd~. */
+void orc_simulate(const double *mean, const double *var, int64_t nstar, int32_t n_sim,
+                  uint64_t seed, double z_crit, double *sim_mean, double *sim_sd, double *lo,
+                  double *hi) {
+  for (int64_t j = 0; j < nstar; j++) {
+    const double sd = sqrt(var[j]);
+    double sum = 0.0;
+    double *x = (double *)malloc(sizeof(double) * n_sim);
+    for (int32_t s2 = 0; s2 < n_sim; s2++) {
+      const uint64_t c = (uint64_t)j * (uint64_t)n_sim + (uint64_t)s2;
+      const double u1 = ((double)(orc_splitmix64(seed, 2 * c) >> 11) + 0.5) * 0x1p-53;
+      const double u2 = ((double)(orc_splitmix64(seed, 2 * c + 1) >> 11) + 0.5) * 0x1p-53;
+      const double z = sqrt(-2.0 * log(u1)) * cos(2.0 * M_PI * u2);
+      x[s2] = mean[j] + sd * z;
+      sum = sum + x[s2];
+    }
+    const double mu = sum / n_sim;
+    double ss = 0.0;
+    for (int32_t s2 = 0; s2 < n_sim; s2++) ss = ss + (x[s2] - mu) * (x[s2] - mu);
+    free(x);
+    const double sdv = sqrt(ss / (n_sim - 1));
+    sim_mean[j] = mu;
+    sim_sd[j] = sdv;
+    lo[j] = mu - z_crit * sdv;
+    hi[j] = mu + z_crit * sdv;
+  }
+}
+
+/* z_{alpha/2} for a two-sided (1 - alpha) = ci_level interval:
+ * the x with P(Z > x) = erfc(x / sqrt 2) / 2 = alpha / 2, by bisection. */
+double orc_z_crit(double ci_level) {
+  const double tail = 0.5 * (1.0 - ci_level);
+  double lo = 0.0, hi = 40.0;
+  for (int it = 0; it < 200; it++) {
+    const double mid = 0.5 * (lo + hi);
+    if (0.5 * erfc(mid / sqrt(2.0)) > tail)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return 0.5 * (lo + hi);
 }
