@@ -176,6 +176,48 @@ int sbv_last_error(sbv_handle h, int64_t *block, int32_t *stage, const char **ms
 
 int sbv_abi_version(void);
 
+/* ---------------------------------------------------------------------------
+ * Prediction: Eq.3 with the Sec.4.1
+ * conditional per test block, and Sec.5.5 conditional simulation
+ * (P:503-507).  Requires a handle prepared on the TRAINING inputs with the
+ * grid kNN (SBV_GRID unset / 1 and m <= 960).
+ *
+ * sbv_predict: X_star n_star x d row-major FP64 test inputs (host or device),
+ * scaled by the handle's `scale`.  Test blocks: k* = max(1, round(n_star /
+ * bs_pred)) anchors by the handle's seed and nearest-anchor assignment (the
+ * same H2-H5 rules as prepare, on the test set).  Conditioning set of test
+ * block j: the exact m_pred nearest TRAINING points (scaled distance, ties to
+ * the lower index) of its centroid, no ordering constraint.
+ * y: n training observations (host or device); theta as in sbv_loglik.
+ * mean / var: n_star outputs (host or device), in the caller's test order:
+ * mean = Sigma_{*J} Sigma_JJ^{-1} y_J, var = diag(Sigma_** - Sigma_{*J}
+ * Sigma_JJ^{-1} Sigma_{J*}) with the nugget on Sigma_**'s diagonal.
+ * Errors: SBV_ERR_ARG (NULL / ranges / non-finite X_star), SBV_ERR_STATE (not
+ * prepared), SBV_ERR_UNSUPPORTED (no grid kNN, m_pred > 960, or
+ * m_pred + test block > 4096), SBV_ERR_NOT_PD (lowest failing test block in
+ * sbv_last_error).  Single device: every rank predicts every test block. */
+int sbv_predict(sbv_handle h, const double *X_star, int64_t n_star, int32_t bs_pred, int32_t m_pred,
+                const double *y, const double *theta, double *mean, double *var);
+
+/* Structure of the last sbv_predict (any output may be NULL): number of test
+ * blocks, test anchors int32[k*], test point -> block int32[n_star], block
+ * offsets int64[k*+1] and block-major test permutation int32[n_star], and the
+ * conditioning sets int32[k* x m_pred] as ORIGINAL training indices (-1 pad)
+ * with counts int32[k*]. */
+int sbv_get_prediction(sbv_handle h, int64_t *k_star, int32_t *anchors, int32_t *block_of, int64_t *off,
+                       int32_t *perm, int32_t *nbr, int32_t *cnt);
+
+/* Sec.5.5 conditional simulation: for each point j, n_sim draws
+ * x = mean_j + sqrt(var_j) z with z = sqrt(-2 ln u1) cos(2 pi u2), u1, u2 =
+ * ((splitmix64(seed, 2c) >> 11) + 0.5) 2^-53 and ((splitmix64(seed, 2c+1) >>
+ * 11) + 0.5) 2^-53, c = j n_sim + s; outputs the sample mean, the sample sd
+ * (divisor n_sim - 1) and sample mean -/+ z_{alpha/2} sd, alpha = 1 - ci_level.
+ * Inputs / outputs n_star doubles, host or device.  var must be >= 0
+ * (SBV_ERR_ARG otherwise), n_sim >= 2, 0 < ci_level < 1. */
+int sbv_simulate(sbv_handle h, const double *mean, const double *var, int64_t n_star, int32_t n_sim,
+                 uint64_t seed, double ci_level, double *sim_mean, double *sim_sd, double *ci_lo,
+                 double *ci_hi);
+
 #ifdef __cplusplus
 }
 #endif

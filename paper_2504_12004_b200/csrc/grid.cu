@@ -563,15 +563,18 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
     const int64_t *__restrict__ off, const double *__restrict__ C,
     const int32_t *__restrict__ local_blocks, int64_t k_local, int d, int m, KnnLevels lv,
     const int32_t *__restrict__ c_start_all, const int32_t *__restrict__ c_list, int32_t *__restrict__ nbr,
-    int32_t *__restrict__ cnt_out, int wcap) {
+    int32_t *__restrict__ cnt_out, int wcap, const double *__restrict__ Cq, int32_t A_all) {
   extern __shared__ WCand sbuf[];  // kKnnWarps x wcap, then kKnnWarps x 256 histogram bins
   unsigned *hist = reinterpret_cast<unsigned *>(sbuf + kKnnWarps * wcap) + (threadIdx.x >> 5) * 256;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t li = blockIdx.x * (int64_t)kKnnWarps + w;
   if (li >= k_local) return;
   WCand *buf = sbuf + w * wcap;
-  const int64_t t = local_blocks[li];
-  const int32_t A = (int32_t)off[t];  // admissible positions [0, A)
+  // estimation: query = centroid of block t, admissible = strictly earlier
+  // blocks [0, off_t); prediction (Cq): query = test centroid li, all n points
+  const int64_t t = Cq ? li : local_blocks[li];
+  const int32_t A = Cq ? A_all : (int32_t)off[t];  // admissible positions [0, A)
+  const double *Crow = Cq ? Cq + li * d : C + t * d;
   // the smallest prefix level that indexes all of [0, A)
   GridDesc g = lv.g[0];
   int64_t coff = 0;
@@ -584,10 +587,10 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
   const int32_t *__restrict__ c_start = c_start_all + coff;
   double c[DM];
 #pragma unroll
-  for (int j = 0; j < DM; j++) c[j] = j < d ? C[t * d + j] : 0.0;
+  for (int j = 0; j < DM; j++) c[j] = j < d ? Crow[j] : 0.0;
   RingQ q;
   for (int x = 0; x < 3; x++) {
-    q.x[x] = x < g.G ? C[t * d + g.dim[x]] : 0.0;
+    q.x[x] = x < g.G ? Crow[g.dim[x]] : 0.0;
     q.cq[x] = x < g.G ? cell_coord(q.x[x], g.lo[x], g.h[x], g.nc[x]) : 0;
   }
   int count = 0;
@@ -757,7 +760,7 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
 cudaError_t launch_knn_grid(const double *Sperm, const int32_t *perm, const int64_t *off,
                             const double *C, const int32_t *local_blocks, int64_t k_local, int d,
                             int m, const KnnLevels &lv, const int32_t *c_start, const int32_t *c_list,
-                            int32_t *nbr, int32_t *cnt, cudaStream_t st) {
+                            int32_t *nbr, int32_t *cnt, cudaStream_t st, const double *Cq, int32_t A_all) {
   if (k_local == 0) return cudaSuccess;
   if (m == 0) return cudaMemsetAsync(cnt, 0, k_local * 4, st);
   const int grid = (int)((k_local + kKnnWarps - 1) / kKnnWarps);
@@ -771,7 +774,7 @@ cudaError_t launch_knn_grid(const double *Sperm, const int32_t *perm, const int6
   do {                                                                                                  \
     cudaFuncSetAttribute(k_knn_grid<DMv>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);          \
     k_knn_grid<DMv><<<grid, thr, smem, st>>>(Sperm, perm, off, C, local_blocks, k_local, d, m, lv,    \
-                                             c_start, c_list, nbr, cnt, wcap);                         \
+                                             c_start, c_list, nbr, cnt, wcap, Cq, A_all);              \
   } while (0)
   if (d <= 4)
     SBV_KNN(4);

@@ -71,41 +71,67 @@ int h8_max_ctas_per_sm(size_t smem, int d) {
   return best;
 }
 
-cudaError_t launch_h8(const Ctx &c, const double *theta, cudaStream_t st) {
+cudaError_t launch_h8_problem(const H8Problem &pb, int d, const double *theta, unsigned int *queue,
+                              cudaStream_t st) {
   H8Args a;
-  a.Xp = c.Xperm;
-  a.yperm = c.yperm;
-  a.off = c.off;
-  a.nbr = c.nbr;
-  a.cnt = c.cnt;
-  a.local_blocks = c.local_blocks;
-  a.work_order = c.work_order;
-  a.k_local = c.k_local;
-  a.m = c.m > 0 ? c.m : 1;
-  a.d = c.d;
+  a.Xp = pb.Xp;
+  a.yperm = pb.yperm;
+  a.off = pb.off;
+  a.nbr = pb.nbr;
+  a.cnt = pb.cnt;
+  a.local_blocks = pb.local_blocks;
+  a.work_order = pb.work_order;
+  a.k_local = pb.k_local;
+  a.m = pb.m > 0 ? pb.m : 1;
+  a.d = d;
   a.sigma2 = theta[0];
-  a.tau2 = theta[c.d + 2];
-  for (int j = 0; j < SBV_MAX_D; j++) a.inv_beta[j] = j < c.d ? 1.0 / theta[1 + j] : 0.0;
-  a.ws = c.ws;
-  a.ws_per_cta = c.ws_per_cta;
-  a.vs_off = h8_l_doubles(c.max_N);
-  a.queue = c.queue;
-  a.terms = c.terms;
-  a.quads = c.quads;
-  a.logdets = c.logdets;
-  a.status = c.status;
-  a.np_max = h8_np_max(c.max_N);
-  a.max_tasks = h8_max_tasks(c.max_N);
-  const double nu = theta[c.d + 1];
-  cudaError_t e = cudaMemsetAsync(c.queue, 0, sizeof(unsigned int), st);
+  a.tau2 = theta[d + 2];
+  for (int j = 0; j < SBV_MAX_D; j++) a.inv_beta[j] = j < d ? 1.0 / theta[1 + j] : 0.0;
+  a.ws = pb.ws;
+  a.ws_per_cta = pb.ws_per_cta;
+  a.vs_off = h8_l_doubles(pb.max_N);
+  a.queue = queue;
+  a.terms = pb.terms;
+  a.quads = pb.quads;
+  a.logdets = pb.logdets;
+  a.status = pb.status;
+  a.np_max = h8_np_max(pb.max_N);
+  a.max_tasks = h8_max_tasks(pb.max_N);
+  a.predict = pb.predict;
+  a.Xq = pb.Xq;
+  a.pmean = pb.pmean;
+  a.pvar = pb.pvar;
+  const double nu = theta[d + 1];
+  cudaError_t e = cudaMemsetAsync(queue, 0, sizeof(unsigned int), st);
   if (e) return e;
-  if (c.k_local == 0) return cudaSuccess;
-  const int grid = c.h8_grid;
-  const size_t smem = c.h8_smem;
-  const H8Fn f = pick(nu, c.d);
-  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  f<<<grid, kH8Threads, smem, st>>>(a);
+  if (pb.k_local == 0) return cudaSuccess;
+  const H8Fn f = pick(nu, d);
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pb.smem);
+  f<<<pb.grid, kH8Threads, pb.smem, st>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t launch_h8(const Ctx &c, const double *theta, cudaStream_t st) {
+  H8Problem pb{};
+  pb.Xp = c.Xperm;
+  pb.yperm = c.yperm;
+  pb.off = c.off;
+  pb.nbr = c.nbr;
+  pb.cnt = c.cnt;
+  pb.local_blocks = c.local_blocks;
+  pb.work_order = c.work_order;
+  pb.k_local = c.k_local;
+  pb.m = c.m;
+  pb.max_N = c.max_N;
+  pb.grid = c.h8_grid;
+  pb.smem = c.h8_smem;
+  pb.ws = c.ws;
+  pb.ws_per_cta = c.ws_per_cta;
+  pb.terms = c.terms;
+  pb.quads = c.quads;
+  pb.logdets = c.logdets;
+  pb.status = c.status;
+  return launch_h8_problem(pb, c.d, theta, c.queue, st);
 }
 
 }  // namespace sbv

@@ -106,6 +106,27 @@ void free_state(sbv_ctx *h) {
   release(h->p_start);
   release(h->p_list);
   release(h->ws);
+  release(h->Xq);
+  release(h->Sq);
+  release(h->Sqp);
+  release(h->Xqp);
+  release(h->Cq);
+  release(h->q_anchors);
+  release(h->q_block_of);
+  release(h->q_perm);
+  release(h->q_nbr);
+  release(h->q_cnt);
+  release(h->q_local);
+  release(h->q_order);
+  release(h->q_status);
+  release(h->q_off);
+  release(h->qa_start);
+  release(h->qa_list);
+  release(h->q_mean);
+  release(h->q_var);
+  release(h->q_terms);
+  release(h->q_quads);
+  release(h->q_logdets);
   h->cap.clear();
   h->prepared = false;
 }
@@ -158,6 +179,65 @@ __global__ void k_block_of_from_layout(const int32_t *perm, const int64_t *off, 
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < k;
        t += (int64_t)gridDim.x * blockDim.x)
     for (int64_t p = off[t]; p < off[t + 1]; p++) bo[perm[p]] = (int32_t)t;
+}
+
+__global__ void k_iota(int32_t *p, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = (int32_t)i;
+}
+
+// out[perm[p]] = in[p]: block-major -> caller order
+__global__ void k_unpermute(const double *in, const int32_t *perm, int64_t n, double *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[perm[i]] = in[i];
+}
+
+// Sec.5.5 conditional simulation, thread per point:
+// x_s = mean + sqrt(var) z_s, z_s by Box-Muller from splitmix64 counters
+// 2c, 2c+1 (c = j n_sim + s); two passes (mean, then squared deviations).
+__device__ __forceinline__ uint64_t sim_splitmix64(uint64_t seed, uint64_t i) {
+  uint64_t z = seed + (i + 1) * 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double sim_normal(uint64_t seed, uint64_t c) {
+  const double u1 = ((double)(sim_splitmix64(seed, 2 * c) >> 11) + 0.5) * 0x1p-53;
+  const double u2 = ((double)(sim_splitmix64(seed, 2 * c + 1) >> 11) + 0.5) * 0x1p-53;
+  return sqrt(-2.0 * log(u1)) * cos(2.0 * M_PI * u2);
+}
+__global__ void k_simulate(const double *mean, const double *var, int64_t ns, int n_sim, uint64_t seed,
+                           double ci_level, double *sm, double *ssd, double *lo, double *hi) {
+  // z_{alpha/2}: P(Z > z) = erfc(z / sqrt 2) / 2 = (1 - ci) / 2, by bisection
+  const double tail = 0.5 * (1.0 - ci_level);
+  double zl = 0.0, zh = 40.0;
+  for (int it = 0; it < 200; it++) {
+    const double mid = 0.5 * (zl + zh);
+    if (0.5 * erfc(mid / sqrt(2.0)) > tail)
+      zl = mid;
+    else
+      zh = mid;
+  }
+  const double zc = 0.5 * (zl + zh);
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < ns;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const double mu = mean[j], sd = sqrt(var[j]);
+    double sum = 0.0;
+    for (int s = 0; s < n_sim; s++) sum = sum + (mu + sd * sim_normal(seed, (uint64_t)j * n_sim + s));
+    const double xm = sum / n_sim;
+    double ss = 0.0;
+    for (int s = 0; s < n_sim; s++) {
+      const double dv = (mu + sd * sim_normal(seed, (uint64_t)j * n_sim + s)) - xm;
+      ss = ss + dv * dv;
+    }
+    const double sdv = sqrt(ss / (n_sim - 1));
+    sm[j] = xm;
+    ssd[j] = sdv;
+    lo[j] = xm - zc * sdv;
+    hi[j] = xm + zc * sdv;
+  }
 }
 
 int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); }
@@ -362,6 +442,8 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
     if (!(scale[j] > 0) || !isfinite(scale[j])) return fail(h, SBV_ERR_ARG, "scale_j must be finite and > 0");
   CU(cudaSetDevice(h->device));
   h->prepared = false;
+  h->lv_valid = false;
+  h->ks = 0;
   h->n = n;
   h->d = d;
   h->bs = bs;
@@ -469,6 +551,8 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
     CU(ensure(h->p_start, lv.cell_off[lv.nl] + 1, unused));
     CU(ensure(h->p_list, lv.list_off[lv.nl], unused));
     CU(build_knn_levels(h->Sperm, d, lv, h->p_start, h->p_list, st));
+    h->lv = lv;
+    h->lv_valid = true;
     tm.mark("H6_grid");
     CU(launch_knn_grid(h->Sperm, h->perm, h->off, h->C, h->local_blocks, h->k_local, d, m, lv,
                        h->p_start, h->p_list, h->nbr, h->cnt, st));
@@ -704,6 +788,230 @@ int sbv_last_error(sbv_handle h, int64_t *block, int32_t *stage, const char **ms
   if (block) *block = h->err_block;
   if (stage) *stage = h->err_stage;
   if (msg) *msg = h->err_msg.c_str();
+  return SBV_OK;
+}
+
+
+// ------------------------------------------------------------------ prediction (N2)
+// Eq.3 with Sec.4.1 per test block and
+// Sec.5.5.  Test blocks: the same anchors + RAC (H2-H5) on the
+// scaled test inputs; conditioning sets: exact m_pred-NN of the test-block
+// centroid over ALL training points (prediction mode) on the training
+// grid levels built by prepare; per block: the fused H8 kernel in prediction
+// mode (border values 0 on the test rows), whose epilogue reads mean and
+// variance off the factor.
+int sbv_predict(sbv_handle h, const double *Xs, int64_t ns, int32_t bs_pred, int32_t m_pred,
+                const double *y, const double *theta, double *mean, double *var) {
+  if (!h) return SBV_ERR_ARG;
+  if (!h->prepared) return fail(h, SBV_ERR_STATE, "sbv_predict before sbv_prepare");
+  if (!Xs || !y || !mean || !var) return fail(h, SBV_ERR_ARG, "NULL argument");
+  if (ns < 1 || ns >= (int64_t(1) << 31)) return fail(h, SBV_ERR_ARG, "n_star out of range");
+  if (bs_pred < 1 || bs_pred > ns) return fail(h, SBV_ERR_ARG, "bs_pred out of range [1, n_star]");
+  if (m_pred < 0) return fail(h, SBV_ERR_ARG, "m_pred must be >= 0");
+  if (!h->lv_valid || m_pred > knn_grid_max_m())
+    return fail(h, SBV_ERR_UNSUPPORTED, "prediction needs the grid kNN (SBV_GRID=1, m, m_pred <= 960)");
+  int rc = validate_theta(h, theta);
+  if (rc) return rc;
+  CU(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  auto &cap = h->cap;
+  const int d = h->d;
+  const int64_t n = h->n;
+  const int64_t ks = std::max<int64_t>(1, (2 * ns + bs_pred) / (2 * (int64_t)bs_pred));
+  h->ns = ns;
+  h->ks = ks;
+  h->bs_pred = bs_pred;
+  h->m_pred = m_pred;
+  // test inputs: device memory read in place, host memory staged
+  const double *Xd = Xs;
+  if (!is_device_ptr(Xs)) {
+    CU(ensure(h->Xq, ns * d, cap));
+    CU(cudaMemcpyAsync(h->Xq, Xs, ns * d * sizeof(double), cudaMemcpyHostToDevice, st));
+    Xd = h->Xq;
+  }
+  CU(cudaMemsetAsync(h->flag, 0, sizeof(int), st));
+  k_check_finite<<<grid_for(ns * d), 256, 0, st>>>(Xd, ns * d, h->flag);
+  CU(cudaMemcpyAsync(h->flag_host, h->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CU(ensure(h->Sq, ns * d, cap));
+  CU(launch_scale(Xd, ns, d, h->scale.data(), h->Sq, st));
+  // test blocks: anchors (same seed), grid RAC, layout, centroids
+  CU(ensure(h->q_anchors, ks, cap));
+  CU(select_anchors_fast(ns, ks, h->seed, h->q_anchors, h->flag + 1, st));
+  CU(cudaMemcpyAsync(h->flag_host + 1, h->flag + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  double lo_hi[2 * SBV_MAX_D];
+  CU(data_extents(h->Sq, ns, d, lo_hi, st));
+  if (*h->flag_host) return fail(h, SBV_ERR_ARG, "X_star has non-finite entries");
+  if (h->flag_host[1] != 0) CU(select_anchors(ns, ks, h->seed, h->q_anchors, nullptr, 0, st, nullptr));
+  const GridDesc ga = make_grid(lo_hi, d, ks, 3.0);
+  CU(ensure(h->qa_start, ga.ncells + 1, cap));
+  CU(ensure(h->qa_list, ks, cap));
+  CU(build_cells(h->Sq, h->q_anchors, ks, d, ga, h->qa_start, h->qa_list, st));
+  CU(ensure(h->q_block_of, ns, cap));
+  CU(launch_rac_grid(h->Sq, ns, 0, d, h->q_anchors, ks, ga, h->qa_start, h->qa_list, h->q_block_of, st));
+  CU(anchor_own_block(h->q_anchors, ks, h->q_block_of, st));
+  CU(ensure(h->q_perm, ns, cap));
+  CU(ensure(h->q_off, ks + 1, cap));
+  CU(build_layout(h->q_block_of, ns, ks, h->q_perm, h->q_off, nullptr, 0, st, nullptr));
+  CU(ensure(h->Sqp, ns * d, cap));
+  CU(launch_gather_rows(h->Sq, h->q_perm, ns, d, h->Sqp, st));
+  CU(ensure(h->Xqp, ns * d, cap));
+  CU(launch_gather_rows(Xd, h->q_perm, ns, d, h->Xqp, st));
+  CU(ensure(h->Cq, ks * d, cap));
+  CU(launch_centroids(h->Sqp, h->q_off, nullptr, ks, d, h->Cq, st));
+  // prediction-mode NN over all n training points
+  const int mm = m_pred > 0 ? m_pred : 1;
+  CU(ensure(h->q_local, ks, cap));
+  k_iota<<<grid_for(ks), 256, 0, st>>>(h->q_local, ks);
+  CU(ensure(h->q_nbr, ks * mm, cap));
+  CU(ensure(h->q_cnt, ks, cap));
+  CU(launch_knn_grid(h->Sperm, h->perm, h->off, h->C, h->q_local, ks, d, m_pred, h->lv, h->p_start,
+                     h->p_list, h->q_nbr, h->q_cnt, st, h->Cq, (int32_t)n));
+  // training observations in block-major order (H7)
+  const double *yd = y;
+  if (!is_device_ptr(y)) {
+    CU(cudaMemcpyAsync(h->ybuf, y, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    yd = h->ybuf;
+  }
+  CU(launch_stage_eval(yd, h->perm, n, h->yperm, st));
+  // sizes -> LPT order, launch geometry
+  std::vector<int64_t> qoff(ks + 1);
+  std::vector<int32_t> qcnt(ks), order(ks);
+  CU(cudaMemcpyAsync(qoff.data(), h->q_off, (ks + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(qcnt.data(), h->q_cnt, ks * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  int32_t maxN = 1;
+  std::vector<int32_t> Nt(ks);
+  for (int64_t t = 0; t < ks; t++) {
+    Nt[t] = qcnt[t] + (int32_t)(qoff[t + 1] - qoff[t]);
+    maxN = std::max(maxN, Nt[t]);
+  }
+  if (maxN > 4096) return fail(h, SBV_ERR_UNSUPPORTED, "m_pred + test block size > 4096");
+  {
+    std::vector<int64_t> bucket((size_t)maxN + 2, 0);
+    for (int64_t t = 0; t < ks; t++) bucket[maxN - Nt[t] + 1]++;
+    for (size_t b = 1; b < bucket.size(); b++) bucket[b] += bucket[b - 1];
+    for (int64_t t = 0; t < ks; t++) order[bucket[maxN - Nt[t]]++] = (int32_t)t;
+  }
+  h->max_N_pred = maxN;
+  CU(ensure(h->q_order, ks, cap));
+  CU(cudaMemcpyAsync(h->q_order, order.data(), ks * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  const size_t smem = h8_smem_bytes(maxN, d);
+  int smem_optin = 0, sms = 0;
+  CU(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+  if (smem + 1024 > (size_t)smem_optin)
+    return fail(h, SBV_ERR_UNSUPPORTED, "test block + neighbour set too large for shared memory staging");
+  const int per_sm = std::max(1, h8_max_ctas_per_sm(smem, d));
+  const int grid = (int)std::min<int64_t>((int64_t)sms * per_sm, ks);
+  const size_t ws_per_cta = h8_ws_doubles(maxN, d);
+  CU(ensure(h->ws, (size_t)grid * ws_per_cta, cap));
+  CU(ensure(h->q_mean, ns, cap));
+  CU(ensure(h->q_var, ns, cap));
+  CU(ensure(h->q_terms, ks, cap));
+  CU(ensure(h->q_quads, ks, cap));
+  CU(ensure(h->q_logdets, ks, cap));
+  CU(ensure(h->q_status, ks, cap));
+  CU(ensure(h->queue, 1, cap));
+  H8Problem pb{};
+  pb.Xp = h->Xperm;
+  pb.yperm = h->yperm;
+  pb.off = h->q_off;
+  pb.nbr = h->q_nbr;
+  pb.cnt = h->q_cnt;
+  pb.local_blocks = h->q_local;
+  pb.work_order = h->q_order;
+  pb.k_local = ks;
+  pb.m = m_pred;
+  pb.max_N = maxN;
+  pb.grid = grid;
+  pb.smem = smem;
+  pb.ws = h->ws;
+  pb.ws_per_cta = ws_per_cta;
+  pb.terms = h->q_terms;
+  pb.quads = h->q_quads;
+  pb.logdets = h->q_logdets;
+  pb.status = h->q_status;
+  pb.predict = 1;
+  pb.Xq = h->Xqp;
+  pb.pmean = h->q_mean;
+  pb.pvar = h->q_var;
+  CU(launch_h8_problem(pb, d, theta, h->queue, st));
+  // caller order
+  double *tmp = nullptr;
+  CU(cudaMallocAsync(&tmp, 2 * ns * sizeof(double), st));
+  k_unpermute<<<grid_for(ns), 256, 0, st>>>(h->q_mean, h->q_perm, ns, tmp);
+  k_unpermute<<<grid_for(ns), 256, 0, st>>>(h->q_var, h->q_perm, ns, tmp + ns);
+  CU(cudaMemcpyAsync(mean, tmp, ns * sizeof(double), cudaMemcpyDefault, st));
+  CU(cudaMemcpyAsync(var, tmp + ns, ns * sizeof(double), cudaMemcpyDefault, st));
+  std::vector<int32_t> status(ks);
+  CU(cudaMemcpyAsync(status.data(), h->q_status, ks * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CU(cudaFreeAsync(tmp, st));
+  CU(cudaStreamSynchronize(st));
+  for (int64_t t = 0; t < ks; t++)
+    if (status[t] == 1) {  // Sigma_JJ not positive definite (the B x B factor is unused)
+      h->err_block = t;
+      h->err_stage = status[t];
+      return fail(h, SBV_ERR_NOT_PD, "Cholesky failed in a test block (lowest index in err_block)");
+    }
+  return SBV_OK;
+}
+
+int sbv_get_prediction(sbv_handle h, int64_t *ks, int32_t *anchors, int32_t *block_of, int64_t *off,
+                       int32_t *perm, int32_t *nbr, int32_t *cnt) {
+  if (!h) return SBV_ERR_ARG;
+  if (h->ks == 0) return fail(h, SBV_ERR_STATE, "no sbv_predict on this handle");
+  if (ks) *ks = h->ks;
+  int rc;
+  if ((rc = copy_out(h, anchors, h->q_anchors, h->ks * sizeof(int32_t)))) return rc;
+  if ((rc = copy_out(h, block_of, h->q_block_of, h->ns * sizeof(int32_t)))) return rc;
+  if ((rc = copy_out(h, off, h->q_off, (h->ks + 1) * sizeof(int64_t)))) return rc;
+  if ((rc = copy_out(h, perm, h->q_perm, h->ns * sizeof(int32_t)))) return rc;
+  if (nbr || cnt) {  // conditioning sets as ORIGINAL training indices (-1 padded)
+    cudaStream_t st = h->stream;
+    const int mp = h->m_pred;
+    int32_t *tn = nullptr, *tc = nullptr;
+    CU(cudaMallocAsync(&tn, std::max<int64_t>(h->ks * mp, 1) * sizeof(int32_t), st));
+    CU(cudaMallocAsync(&tc, h->ks * sizeof(int32_t), st));
+    k_nbr_to_orig<<<grid_for(std::max<int64_t>(h->ks * mp, h->ks)), 256, 0, st>>>(
+        h->q_nbr, h->q_cnt, h->perm, h->q_local, h->ks, mp, tn, tc);
+    if ((rc = copy_out(h, nbr, tn, h->ks * mp * sizeof(int32_t)))) return rc;
+    if ((rc = copy_out(h, cnt, tc, h->ks * sizeof(int32_t)))) return rc;
+    cudaFreeAsync(tn, st);
+    cudaFreeAsync(tc, st);
+  }
+  return SBV_OK;
+}
+
+int sbv_simulate(sbv_handle h, const double *mean, const double *var, int64_t ns, int32_t n_sim,
+                 uint64_t seed, double ci_level, double *sim_mean, double *sim_sd, double *ci_lo,
+                 double *ci_hi) {
+  if (!h) return SBV_ERR_ARG;
+  if (!mean || !var || !sim_mean || !sim_sd || !ci_lo || !ci_hi) return fail(h, SBV_ERR_ARG, "NULL argument");
+  if (ns < 1 || n_sim < 2) return fail(h, SBV_ERR_ARG, "n_star >= 1 and n_sim >= 2 required");
+  if (!(ci_level > 0.0 && ci_level < 1.0)) return fail(h, SBV_ERR_ARG, "ci_level must be in (0, 1)");
+  CU(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  double *buf = nullptr;
+  CU(cudaMallocAsync(&buf, 6 * ns * sizeof(double), st));
+  CU(cudaMemcpyAsync(buf, mean, ns * sizeof(double), cudaMemcpyDefault, st));
+  CU(cudaMemcpyAsync(buf + ns, var, ns * sizeof(double), cudaMemcpyDefault, st));
+  std::vector<double> vh(ns);
+  CU(cudaMemcpyAsync(vh.data(), buf + ns, ns * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  for (int64_t j = 0; j < ns; j++)
+    if (!(vh[j] >= 0.0)) {
+      cudaFreeAsync(buf, st);
+      return fail(h, SBV_ERR_ARG, "negative or NaN variance (clamp tiny negatives upstream)");
+    }
+  k_simulate<<<grid_for(ns), 128, 0, st>>>(buf, buf + ns, ns, n_sim, seed, ci_level, buf + 2 * ns,
+                                           buf + 3 * ns, buf + 4 * ns, buf + 5 * ns);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(sim_mean, buf + 2 * ns, ns * sizeof(double), cudaMemcpyDefault, st));
+  CU(cudaMemcpyAsync(sim_sd, buf + 3 * ns, ns * sizeof(double), cudaMemcpyDefault, st));
+  CU(cudaMemcpyAsync(ci_lo, buf + 4 * ns, ns * sizeof(double), cudaMemcpyDefault, st));
+  CU(cudaMemcpyAsync(ci_hi, buf + 5 * ns, ns * sizeof(double), cudaMemcpyDefault, st));
+  CU(cudaFreeAsync(buf, st));
+  CU(cudaStreamSynchronize(st));
   return SBV_OK;
 }
 

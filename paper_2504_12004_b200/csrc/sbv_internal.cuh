@@ -17,6 +17,29 @@ constexpr int kPanel = 32;       // H8 panel width (columns per left-looking ste
 constexpr int kChunkBlocks = 64; // blocks per reduction / shard chunk
 constexpr int kMaxStages = 16;
 
+// ---- grid-filtered exact search (grid.cu): geometry types
+struct GridDesc {
+  int G;          // grid dimensions (<= 3): the scaled dims of largest extent
+  int dim[3];     // which input dimensions
+  double lo[3];   // data minimum per grid dim
+  double h[3];    // cell edge per grid dim
+  int nc[3];      // cells per grid dim
+  int stride[3];  // linear cell index strides
+  int64_t ncells;
+};
+// Prefix-level grids for the kNN (H6): level l buckets the block-major
+// positions [0, P[l]) (P halves from n), so a query whose admissible prefix is
+// [0, A) searches the smallest level with P >= A, where at least half of the
+// indexed points are admissible.  All levels share one list / start array.
+constexpr int kMaxLevels = 16;
+struct KnnLevels {
+  int nl;
+  int32_t direct_max;               // prefixes A <= direct_max are scanned directly
+  int32_t P[kMaxLevels];            // decreasing
+  int64_t cell_off[kMaxLevels + 1]; // level l cells start at cell_off[l] in `start`
+  int64_t list_off[kMaxLevels + 1]; // level l items occupy list[list_off[l], list_off[l+1])
+  GridDesc g[kMaxLevels];
+};
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -73,6 +96,17 @@ struct Ctx {
   size_t occ_smem = 0;  // cached occupancy query
   int occ_per_sm = 0;
   int occ_d = 0;
+  KnnLevels lv{};                 // kNN prefix-level grids of the training set (prepare)
+  bool lv_valid = false;
+  // prediction state (sbv_predict)
+  int64_t ns = 0, ks = 0;         // test points, test blocks
+  int32_t bs_pred = 0, m_pred = 0, max_N_pred = 0;
+  double *Xq = nullptr, *Sq = nullptr, *Sqp = nullptr, *Xqp = nullptr, *Cq = nullptr;
+  int32_t *q_anchors = nullptr, *q_block_of = nullptr, *q_perm = nullptr, *q_nbr = nullptr, *q_cnt = nullptr;
+  int32_t *q_local = nullptr, *q_order = nullptr, *q_status = nullptr;
+  int64_t *q_off = nullptr;
+  int32_t *qa_start = nullptr, *qa_list = nullptr;
+  double *q_mean = nullptr, *q_var = nullptr, *q_terms = nullptr, *q_quads = nullptr, *q_logdets = nullptr;
   std::unordered_map<void *, size_t> cap;  // device buffer capacities (bytes)
   // errors
   int64_t err_block = -1;
@@ -86,28 +120,6 @@ struct Ctx {
 };
 
 // ---- grid-filtered exact search (grid.cu)
-struct GridDesc {
-  int G;          // grid dimensions (<= 3): the scaled dims of largest extent
-  int dim[3];     // which input dimensions
-  double lo[3];   // data minimum per grid dim
-  double h[3];    // cell edge per grid dim
-  int nc[3];      // cells per grid dim
-  int stride[3];  // linear cell index strides
-  int64_t ncells;
-};
-// Prefix-level grids for the kNN (H6): level l buckets the block-major
-// positions [0, P[l]) (P halves from n), so a query whose admissible prefix is
-// [0, A) searches the smallest level with P >= A, where at least half of the
-// indexed points are admissible.  All levels share one list / start array.
-constexpr int kMaxLevels = 16;
-struct KnnLevels {
-  int nl;
-  int32_t direct_max;               // prefixes A <= direct_max are scanned directly
-  int32_t P[kMaxLevels];            // decreasing
-  int64_t cell_off[kMaxLevels + 1]; // level l cells start at cell_off[l] in `start`
-  int64_t list_off[kMaxLevels + 1]; // level l items occupy list[list_off[l], list_off[l+1])
-  GridDesc g[kMaxLevels];
-};
 KnnLevels make_knn_levels(const double *lo_hi, int d, int64_t n, int m);
 cudaError_t build_knn_levels(const double *Sperm, int d, const KnnLevels &lv, int32_t *start,
                              int32_t *list, cudaStream_t st);
@@ -121,7 +133,8 @@ cudaError_t launch_rac_grid(const double *S, int64_t n, int64_t i0, int d, const
 cudaError_t launch_knn_grid(const double *Sperm, const int32_t *perm, const int64_t *off,
                             const double *C, const int32_t *local_blocks, int64_t k_local, int d,
                             int m, const KnnLevels &lv, const int32_t *c_start, const int32_t *c_list,
-                            int32_t *nbr, int32_t *cnt, cudaStream_t st);
+                            int32_t *nbr, int32_t *cnt, cudaStream_t st, const double *Cq = nullptr,
+                            int32_t A_all = 0);
 int knn_grid_max_m();
 cudaError_t anchor_own_block(const int32_t *anchors, int64_t k, int32_t *block_of, cudaStream_t st);
 
@@ -152,6 +165,25 @@ size_t h8_smem_bytes(int max_N, int d);
 size_t h8_ws_doubles(int max_N, int d);
 int h8_max_ctas_per_sm(size_t smem, int d);
 cudaError_t launch_h8(const Ctx &c, const double *theta_host, cudaStream_t st);
+// One H8 launch over an explicit set of blocks (estimation or prediction mode)
+struct H8Problem {
+  const double *Xp, *yperm;        // training inputs / observations, block-major
+  const int64_t *off;              // block offsets (training blocks, or test blocks in prediction)
+  const int32_t *nbr, *cnt;        // conditioning sets (training block-major positions)
+  const int32_t *local_blocks, *work_order;
+  int64_t k_local;
+  int m, max_N, grid;
+  size_t smem;
+  double *ws;
+  size_t ws_per_cta;
+  double *terms, *quads, *logdets;
+  int32_t *status;
+  int predict;                     // 1: B rows are test points Xq, outputs pmean / pvar
+  const double *Xq;
+  double *pmean, *pvar;
+};
+cudaError_t launch_h8_problem(const H8Problem &pb, int d, const double *theta_host, unsigned int *queue,
+                              cudaStream_t st);
 cudaError_t launch_reduce_chunks(const Ctx &c, cudaStream_t st);
 cudaError_t launch_final_reduce(const Ctx &c, cudaStream_t st);
 

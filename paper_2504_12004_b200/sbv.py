@@ -42,7 +42,8 @@ EXPORTS = ["sbv_abi_version", "sbv_create", "sbv_destroy", "sbv_comm_unique_id",
            "sbv_shard_blocks",
            "sbv_prepare_h", "sbv_prepare_ex", "sbv_prepare", "sbv_loglik", "sbv_loglik_parts",
            "sbv_block_terms", "sbv_num_blocks", "sbv_get_anchors", "sbv_get_blocks",
-           "sbv_get_neighbors", "sbv_stats", "sbv_stage_times", "sbv_last_error"]
+           "sbv_get_neighbors", "sbv_stats", "sbv_stage_times", "sbv_last_error",
+           "sbv_predict", "sbv_get_prediction", "sbv_simulate"]
 
 
 def lib():
@@ -74,6 +75,10 @@ def lib():
         L.sbv_stage_times.argtypes = [_p, _i32, _p, _p, _i32, ctypes.POINTER(_i32)]
         L.sbv_last_error.argtypes = [_p, ctypes.POINTER(_i64), ctypes.POINTER(_i32),
                                      ctypes.POINTER(ctypes.c_char_p)]
+        L.sbv_predict.argtypes = [_p, _p, _i64, _i32, _i32, _p, _p, _p, _p]
+        L.sbv_get_prediction.argtypes = [_p, ctypes.POINTER(_i64), _p, _p, _p, _p, _p, _p]
+        L.sbv_simulate.argtypes = [_p, _p, _p, _i64, _i32, ctypes.c_uint64, ctypes.c_double,
+                                   _p, _p, _p, _p]
         _lib = L
     return _lib
 
@@ -221,6 +226,53 @@ class Handle:
         self._check(lib().sbv_get_blocks(self._h, bo.ctypes.data_as(_p), off.ctypes.data_as(_p),
                                          perm.ctypes.data_as(_p), C.ctypes.data_as(_p)))
         return bo, off, perm, C
+
+    # -- prediction
+    def predict(self, X_star, bs_pred: int, m_pred: int, y, theta):
+        """Conditional mean and variance at X_star (Eq.3 / Sec.4.1 per test block).
+        Outputs are numpy arrays unless X_star is a CUDA tensor (then tensors)."""
+        Xs = _f64(X_star)
+        y = _f64(y)
+        th = np.ascontiguousarray(theta, dtype=np.float64)
+        ns = Xs.shape[0]
+        if hasattr(Xs, "data_ptr") and Xs.is_cuda:
+            import torch
+            mean = torch.empty(ns, dtype=torch.float64, device=Xs.device)
+            var = torch.empty(ns, dtype=torch.float64, device=Xs.device)
+        else:
+            mean, var = np.empty(ns), np.empty(ns)
+        px, _k1 = _ptr(Xs)
+        py, _k2 = _ptr(y)
+        pm, _k3 = _ptr(mean)
+        pv, _k4 = _ptr(var)
+        self._check(lib().sbv_predict(self._h, px, ns, bs_pred, m_pred, py, th.ctypes.data_as(_p), pm, pv))
+        self._last_pred = (ns, m_pred)
+        return mean, var
+
+    def prediction_structure(self):
+        """(anchors, block_of, off, perm, nbr (original training indices), cnt) of the last predict."""
+        ks = _i64(0)
+        self._check(lib().sbv_get_prediction(self._h, ctypes.byref(ks), None, None, None, None, None, None))
+        k = ks.value
+        ns, mp = self._last_pred
+        anc = np.empty(k, np.int32)
+        bo = np.empty(ns, np.int32)
+        off = np.empty(k + 1, np.int64)
+        perm = np.empty(ns, np.int32)
+        nbr = np.empty((k, max(mp, 1)), np.int32)
+        cnt = np.empty(k, np.int32)
+        self._check(lib().sbv_get_prediction(self._h, ctypes.byref(ks), *[a.ctypes.data_as(_p) for a in
+                                                                         (anc, bo, off, perm, nbr, cnt)]))
+        return anc, bo, off, perm, nbr[:, :mp], cnt
+
+    def simulate(self, mean, var, n_sim: int, seed: int, ci_level: float = 0.95):
+        """Sec.5.5 conditional simulation: (sample mean, sample sd, ci_lo, ci_hi)."""
+        m = np.ascontiguousarray(mean.cpu().numpy() if hasattr(mean, "cpu") else mean, dtype=np.float64)
+        v = np.ascontiguousarray(var.cpu().numpy() if hasattr(var, "cpu") else var, dtype=np.float64)
+        outs = [np.empty(m.shape[0]) for _ in range(4)]
+        self._check(lib().sbv_simulate(self._h, m.ctypes.data_as(_p), v.ctypes.data_as(_p), m.shape[0],
+                                       n_sim, seed, ci_level, *[o.ctypes.data_as(_p) for o in outs]))
+        return tuple(outs)
 
     def neighbors(self):
         k = self.num_blocks()
