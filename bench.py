@@ -300,6 +300,31 @@ def run_ours(args):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_ms_max = float(te.item())
 
+    # --- NEXT row N2 (prediction), outside the timed step: 100k test points,
+    # bs_pred = 10, m_pred = m on the prepared training set; then Sec.5.5
+    # conditional simulation with 1000 draws per point
+    pred = None
+    if world == 1 and not args.no_predict:
+        ns = 100_000
+        Xs = torch.from_numpy(si.make_X(ns, d, seed=5)).to(dev)
+        h.predict(Xs, 10, m, y, theta)
+        torch.cuda.synchronize()
+        pm = []
+        for _ in range(3):
+            flush.zero_()
+            a.record(stream)
+            mean_p, var_p = h.predict(Xs, 10, m, y, theta)
+            b.record(stream)
+            torch.cuda.synchronize()
+            pm.append(a.elapsed_time(b))
+        t0 = time.perf_counter()
+        h.simulate(mean_p, var_p, 1000, 7, 0.95)
+        sim_ms = (time.perf_counter() - t0) * 1e3
+        pred = {"n_star": ns, "bs_pred": 10, "m_pred": m, "ms": statistics.mean(pm),
+                "points_per_s": ns / (statistics.mean(pm) * 1e-3),
+                "simulate_1000_draws_ms_wall": sim_ms,
+                "note": "includes test clustering, prediction-mode kNN over the 1M training points and the fused conditional kernel"}
+
     # --- kernel launches in one step (CUPTI via torch.profiler, outside the timed region)
     launches = None
     try:
@@ -346,6 +371,7 @@ def run_ours(args):
             "e2e": {"value": 1e3 / e2e_ms_max, "unit": "evals/s",
                     "h2d_bytes_per_step": int(n * d * 8 + n * 8), "d2h_bytes_per_step": 8 * 8},
             "gpu_launches": launches,
+            **({"predict": pred} if pred else {}),
             "clocks": ck,
             "ll": ll,
             "realised": stats,
@@ -422,6 +448,7 @@ def main():
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--ref-sample", type=int, default=400_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-predict", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
