@@ -51,12 +51,12 @@ size_t h8_ws_doubles(int max_N, int d) {
   return h8_l_doubles(max_N) + vs;
 }
 
-static H8Fn pick(double nu, int d) {
+static H8Fn pick(double nu, int d, int pred = 0) {
   const int dm = h8_dm(d);
-  if (nu == 0.5) return h8_pick_nu1(dm);
-  if (nu == 1.5) return h8_pick_nu3(dm);
-  if (nu == 2.5) return h8_pick_nu5(dm);
-  return h8_pick_nu7(dm);
+  if (nu == 0.5) return h8_pick_nu1(dm, pred);
+  if (nu == 1.5) return h8_pick_nu3(dm, pred);
+  if (nu == 2.5) return h8_pick_nu5(dm, pred);
+  return h8_pick_nu7(dm, pred);
 }
 
 int h8_max_ctas_per_sm(size_t smem, int d) {
@@ -105,7 +105,7 @@ cudaError_t launch_h8_problem(const H8Problem &pb, int d, const double *theta, u
   cudaError_t e = cudaMemsetAsync(queue, 0, sizeof(unsigned int), st);
   if (e) return e;
   if (pb.k_local == 0) return cudaSuccess;
-  const H8Fn f = pick(nu, d);
+  const H8Fn f = pick(nu, d, pb.predict);
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pb.smem);
   f<<<pb.grid, kH8Threads, pb.smem, st>>>(a);
   return cudaGetLastError();

@@ -4,15 +4,18 @@
 
 namespace sbv {
 
-H8Fn h8_pick_nu1(int dm) {
+template <int PRED>
+static H8Fn pick_dm(int dm) {
   switch (dm) {
-    case 4: return k_h8<1, 4>;
-    case 8: return k_h8<1, 8>;
-    case 10: return k_h8<1, 10>;
-    case 12: return k_h8<1, 12>;
-    case 16: return k_h8<1, 16>;
-    default: return k_h8<1, 0>;
+    case 4: return k_h8<1, 4, PRED>;
+    case 8: return k_h8<1, 8, PRED>;
+    case 10: return k_h8<1, 10, PRED>;
+    case 12: return k_h8<1, 12, PRED>;
+    case 16: return k_h8<1, 16, PRED>;
+    default: return k_h8<1, 0, PRED>;
   }
 }
+
+H8Fn h8_pick_nu1(int dm, int pred) { return pred ? pick_dm<1>(dm) : pick_dm<0>(dm); }
 
 }  // namespace sbv

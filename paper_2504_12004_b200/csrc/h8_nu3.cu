@@ -4,15 +4,18 @@
 
 namespace sbv {
 
-H8Fn h8_pick_nu3(int dm) {
+template <int PRED>
+static H8Fn pick_dm(int dm) {
   switch (dm) {
-    case 4: return k_h8<3, 4>;
-    case 8: return k_h8<3, 8>;
-    case 10: return k_h8<3, 10>;
-    case 12: return k_h8<3, 12>;
-    case 16: return k_h8<3, 16>;
-    default: return k_h8<3, 0>;
+    case 4: return k_h8<3, 4, PRED>;
+    case 8: return k_h8<3, 8, PRED>;
+    case 10: return k_h8<3, 10, PRED>;
+    case 12: return k_h8<3, 12, PRED>;
+    case 16: return k_h8<3, 16, PRED>;
+    default: return k_h8<3, 0, PRED>;
   }
 }
+
+H8Fn h8_pick_nu3(int dm, int pred) { return pred ? pick_dm<1>(dm) : pick_dm<0>(dm); }
 
 }  // namespace sbv
