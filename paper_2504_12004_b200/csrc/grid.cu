@@ -320,6 +320,9 @@ __device__ __forceinline__ void for_ring(const GridDesc &g, const RingQ &q, int 
 }
 
 // ------------------------------------------------------------------ H3 RAC
+#ifndef SBV_RAC_SORT_MIN
+#define SBV_RAC_SORT_MIN 0  // visit points in cell order when the slice has at least this many
+#endif
 // Anchor rows gathered in cell order (AC) with their ranks, so a cell's
 // candidates are consecutive rows: no indirection through `anchors`.
 __global__ void k_gather_anchor_rows(const double *__restrict__ S, const int32_t *__restrict__ anchors,
@@ -346,7 +349,7 @@ __global__ void __launch_bounds__(256) k_rac_grid2(const double *__restrict__ S,
                                                    int32_t *__restrict__ block_of) {
   const int64_t tt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (tt >= count) return;
-  const int64_t il = order[tt], i = i0 + il;
+  const int64_t il = order ? order[tt] : tt, i = i0 + il;
   double p[DM];
 #pragma unroll
   for (int j = 0; j < DM; j++) p[j] = j < d ? S[i * d + j] : 0.0;
@@ -398,10 +401,11 @@ cudaError_t launch_rac_grid(const double *S, int64_t n, int64_t i0, int d, const
   if ((e = cudaMallocAsync(&pstart, sizeof(int32_t) * (g.ncells + 1), st))) return e;
   k_gather_anchor_rows<<<(int)std::max<int64_t>(1, std::min<int64_t>((k * d + 255) / 256, 148 * 16)), 256, 0, st>>>(
       S, anchors, a_list, k, d, AC, arank);
-  if ((e = build_cells(S + i0 * d, nullptr, count, d, g, pstart, order, st))) return e;
+  const bool sorted = count >= SBV_RAC_SORT_MIN;
+  if (sorted && (e = build_cells(S + i0 * d, nullptr, count, d, g, pstart, order, st))) return e;
   const int grid = (int)((count + 255) / 256);
 #define SBV_RAC(DMv) \
-  k_rac_grid2<DMv><<<grid, 256, 0, st>>>(S, order, count, i0, d, AC, arank, g, a_start, block_of)
+  k_rac_grid2<DMv><<<grid, 256, 0, st>>>(S, sorted ? order : nullptr, count, i0, d, AC, arank, g, a_start, block_of)
   if (d <= 4)
     SBV_RAC(4);
   else if (d <= 8)
