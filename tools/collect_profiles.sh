@@ -4,7 +4,7 @@
 # and of the kNN kernel.  Outputs land in gpurun_out/ (summarised into profiles/).
 set -o pipefail
 mkdir -p gpurun_out
-CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline"
+CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-predict"
 $CMD > gpurun_out/prof_plain.json 2> gpurun_out/prof_plain.err
 rc=$?
 echo "plain rc=$rc"

@@ -37,7 +37,7 @@ def launches(tag):
     tot = sum(v[1] for v in agg.values())
     summary = sorted(({"kernel": k, "launches": c, "total_ms": t / 1e6, "share": t / tot}
                       for k, (c, t) in agg.items()), key=lambda x: -x["total_ms"])
-    return {"command": "python bench.py --steps 3 --warmup 3 --no-cpu-baseline",
+    return {"command": "python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-predict",
             "note": "ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised); "
                     "compare SHARES, not absolute times",
             "total_launches": len(rows), "kernels": summary}
