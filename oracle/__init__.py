@@ -59,6 +59,8 @@ def lib():
         L.orc_knn_block.argtypes = [_p, _i32, _p, _p, _p, _i64, _i32, _p]
         L.orc_knn_block.restype = _i32
         L.orc_knn.argtypes = [_p, _i32, _p, _p, _p, _i64, _i32, _p, _p, _i32]
+        L.orc_besselk.argtypes = [_dbl, _dbl]
+        L.orc_besselk.restype = _dbl
         L.orc_matern.argtypes = [_dbl, _dbl, _dbl]
         L.orc_matern.restype = _dbl
         L.orc_scaled_distance.argtypes = [_p, _p, _i32, _p]
@@ -182,6 +184,10 @@ def knn(S, perm, off, C, m: int, nthreads: int = 0):
 # ----------------------------------------------------------------- O7
 def matern(r: float, sigma2: float, nu: float) -> float:
     return float(lib().orc_matern(r, sigma2, nu))
+
+
+def besselk(nu: float, r: float) -> float:
+    return float(lib().orc_besselk(nu, r))
 
 
 def scaled_distance(xa, xb, beta) -> float:

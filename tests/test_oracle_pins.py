@@ -113,7 +113,28 @@ def test_matern_limits_and_decay(orc, nu):
 
 
 def test_unsupported_nu_is_nan(orc):
-    assert math.isnan(orc.matern(1.0, 1.0, 1.0))
+    assert math.isnan(orc.matern(1.0, 1.0, 0.0))
+    assert math.isnan(orc.matern(1.0, 1.0, -1.0))
+    assert math.isnan(orc.matern(1.0, 1.0, 25.0))
+
+
+@pytest.mark.parametrize("nu", [0.2, 0.5, 0.75, 1.0, 1.3, 2.0, 2.5, 3.7, 6.4])
+def test_besselk_integral_equals_scipy(orc, nu):
+    """N3: the oracle's K_nu (trapezoid on the cosh integral) = scipy.special.kv."""
+    for r in [1e-6, 1e-3, 0.05, 0.3, 1.0, 1.99, 2.01, 5.0, 17.0, 80.0, 300.0]:
+        ref = special.kv(nu, r)
+        assert abs(orc.besselk(nu, r) - ref) <= 1e-13 * ref, (nu, r)
+
+
+@pytest.mark.parametrize("nu", [0.3, 1.0, 2.0, 4.25])
+def test_general_nu_matern_equals_bessel(orc, nu):
+    """N3: Eq.6 for non-half-integer nu = the scipy Bessel form; r=0 limit."""
+    for r in [1e-8, 1e-4, 0.01, 0.5, 1.0, 3.0, 10.0, 50.0]:
+        ref = matern_bessel(np.array(r), 1.7, nu)
+        assert abs(orc.matern(r, 1.7, nu) - ref) <= 1e-12 * max(ref, 1e-300), (nu, r)
+    assert orc.matern(0.0, 1.7, nu) == 1.7
+    # continuity across a half-integer: nu -> 1.5 matches the closed form
+    assert abs(orc.matern(0.8, 1.0, 1.5 + 1e-9) - orc.matern(0.8, 1.0, 1.5)) < 1e-8
 
 
 # --------------------------------------------------------------- O8/O9 likelihood
