@@ -46,7 +46,7 @@ typedef enum {
   SBV_ERR_CUDA = 2,        /* CUDA runtime error or no device */
   SBV_ERR_OOM = 3,         /* device allocation failed */
   SBV_ERR_NOT_PD = 4,      /* a Cholesky pivot was <= 0: see sbv_last_error */
-  SBV_ERR_UNSUPPORTED = 5, /* nu not in {0.5,1.5,2.5,3.5}, or shape beyond kernel limits */
+  SBV_ERR_UNSUPPORTED = 5, /* nu outside (0, 20], or shape beyond kernel limits */
   SBV_ERR_COMM = 6,        /* NCCL failure */
   SBV_ERR_STATE = 7        /* call out of order (e.g. loglik before prepare) */
 } sbv_status;
@@ -121,8 +121,11 @@ int sbv_prepare(const double *X, int64_t n, int32_t d, int32_t bs, int32_t m,
  * nugget tau2 on the diagonal only (Q3).
  * y: length n in original point order (host or device).
  * theta: host double[d+3] = {sigma2, beta_1..beta_d, nu, tau2}.
+ * nu in {0.5, 1.5, 2.5, 3.5} uses the half-integer closed forms (Q4); any
+ * other 0 < nu <= 20 evaluates Eq.6 with K_nu (Temme series / Steed
+ * continued fraction), several times slower per entry.
  * *ll receives ell (NaN on SBV_ERR_NOT_PD).  Synchronous on the stream.
- * Errors: SBV_ERR_ARG (theta invalid), SBV_ERR_UNSUPPORTED (nu),
+ * Errors: SBV_ERR_ARG (theta invalid), SBV_ERR_UNSUPPORTED (nu outside (0, 20]),
  * SBV_ERR_NOT_PD (lowest failing zeta block + stage via sbv_last_error),
  * SBV_ERR_STATE (no prepare), SBV_ERR_CUDA, SBV_ERR_COMM. */
 int sbv_loglik(sbv_handle h, const double *y, const double *theta, double *ll);

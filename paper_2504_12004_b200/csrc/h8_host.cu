@@ -56,12 +56,13 @@ static H8Fn pick(double nu, int d, int pred = 0) {
   if (nu == 0.5) return h8_pick_nu1(dm, pred);
   if (nu == 1.5) return h8_pick_nu3(dm, pred);
   if (nu == 2.5) return h8_pick_nu5(dm, pred);
-  return h8_pick_nu7(dm, pred);
+  if (nu == 3.5) return h8_pick_nu7(dm, pred);
+  return h8_pick_nu0(dm, pred);  // general nu: K_nu path
 }
 
 int h8_max_ctas_per_sm(size_t smem, int d) {
   int best = 1 << 30;
-  for (double nu : {0.5, 1.5, 2.5, 3.5}) {  // the launch may use any smoothness
+  for (double nu : {0.5, 1.5, 2.5, 3.5, 1.0}) {  // the launch may use any smoothness
     const H8Fn f = pick(nu, d);
     int nb = 0;
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -86,6 +87,7 @@ cudaError_t launch_h8_problem(const H8Problem &pb, int d, const double *theta, u
   a.d = d;
   a.sigma2 = theta[0];
   a.tau2 = theta[d + 2];
+  a.nu = theta[d + 1];
   for (int j = 0; j < SBV_MAX_D; j++) a.inv_beta[j] = j < d ? 1.0 / theta[1 + j] : 0.0;
   a.ws = pb.ws;
   a.ws_per_cta = pb.ws_per_cta;

@@ -285,8 +285,8 @@ int validate_theta(sbv_ctx *h, const double *theta) {
     if (!(theta[1 + j] > 0)) return fail(h, SBV_ERR_ARG, "beta_j must be > 0");
   if (!(theta[d + 2] >= 0)) return fail(h, SBV_ERR_ARG, "tau2 must be >= 0");
   const double nu = theta[d + 1];
-  if (nu != 0.5 && nu != 1.5 && nu != 2.5 && nu != 3.5)
-    return fail(h, SBV_ERR_UNSUPPORTED, "nu must be one of 0.5, 1.5, 2.5, 3.5");
+  if (!(nu > 0.0) || nu > 20.0)
+    return fail(h, SBV_ERR_UNSUPPORTED, "nu must be in (0, 20] (closed forms at 0.5/1.5/2.5/3.5, K_nu otherwise)");
   return SBV_OK;
 }
 

@@ -169,7 +169,7 @@ def test_argument_errors(sbv):
         sbv.prepare(Xn, 10, 5, np.ones(3))
     h = sbv.prepare(X, 10, 5, np.ones(3))
     with pytest.raises(sbv.SBVError) as e:
-        h.loglik(np.zeros(100), np.array([1.0, 1, 1, 1, 1.0, 0.0]))  # nu = 1.0 unsupported
+        h.loglik(np.zeros(100), np.array([1.0, 1, 1, 1, 25.0, 0.0]))  # nu > 20 unsupported
     assert e.value.code == 5
     with pytest.raises(sbv.SBVError) as e:
         h.loglik(np.zeros(100), np.array([-1.0, 1, 1, 1, 2.5, 0.0]))
@@ -241,6 +241,18 @@ def test_cfg2_full_size_sampled(sbv, orc):
     ll = h.loglik(torch.from_numpy(y).cuda(), theta)
     ll_o = orc.loglik(X, y, perm, off, nbr, cnt, theta)
     assert abs(ll - ll_o) <= TOL_LL * max(abs(ll_o), np.abs(terms).sum()), (ll, ll_o)
+
+
+@pytest.mark.parametrize("nu", [0.3, 1.0, 2.0, 4.25])
+def test_parity_general_nu(sbv, orc, nu):
+    """non-half-integer smoothness through the K_nu path."""
+    n, d = 2500, 5
+    X = si.make_X(n, d, seed=90)
+    y = si.make_y(X, seed=91)
+    scale = si.default_scale(d)
+    theta = si.default_theta(d, nu=nu, tau2=1e-3)
+    h, P, Xt, yt = run_both(sbv, orc, X, y, 10, 40, scale, theta)
+    check_terms(h, orc, X, y, yt, P, theta)
 
 
 def test_cfg1_full_size(sbv, orc):
