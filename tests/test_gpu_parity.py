@@ -85,6 +85,19 @@ def test_parity_small(sbv, orc, d, bs, m, nu):
     check_terms(h, orc, X, y, yt, P, theta)
 
 
+@pytest.mark.parametrize("d", [1, 20, 64])
+def test_parity_dimension_edges(sbv, orc, d):
+    """d = 1 and the generic (d > 16) coordinate paths of RAC, kNN and H8, up to SBV_MAX_D."""
+    n = 1500
+    X = si.make_X(n, d, seed=100 + d)
+    y = si.make_y(X, seed=200 + d)
+    scale = np.linspace(0.5, 2.0, d)
+    theta = np.array([1.1, *np.linspace(0.6, 3.0, d), 1.5, 1e-3])
+    h, P, Xt, yt = run_both(sbv, orc, X, y, 15, 35, scale, theta)
+    check_indices(h, P)
+    check_terms(h, orc, X, y, yt, P, theta)
+
+
 def test_parity_large_blocks_multi_pass(sbv, orc):
     """N_t = m + bs up to ~700 rows: several 256-row passes per panel, ragged tails."""
     n, d, bs, m = 4000, 4, 300, 350
