@@ -635,7 +635,9 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   h->h8_grid = (int)std::min<int64_t>((int64_t)sms * per_sm, std::max<int64_t>(h->k_local, 1));
   h->ws_per_cta = h8_ws_doubles(std::max(h->max_N, 1), d);
   CU(ensure(h->ws, (size_t)h->h8_grid * h->ws_per_cta, unused));
-  CU(cudaStreamSynchronize(st));
+  // no trailing host sync: everything above is stream-ordered before the
+  // first sbv_loglik, and the pinned staging is only rewritten after the next
+  // prepare's own first sync
   tm.mark("meta");
   tm.finish();
   h->prepared = true;
