@@ -140,3 +140,43 @@ def test_predict_cfg2_shape_sampled(sbv, orc):
         mo, vo = orc.predict_block(X, y, Xs, J, B, theta)
         assert np.abs(mean[B] - mo).max() <= 1e-9 * max(1.0, np.abs(y).max())
         assert np.abs(var[B] - vo).max() <= 1e-9 * (theta[0] + theta[d + 2])
+
+
+def test_predict_and_simulate_argument_errors(sbv):
+    X = si.make_X(500, 3, seed=1)
+    y = si.make_y(X, seed=2)
+    theta = si.default_theta(3, nu=2.5)
+    h = sbv.Handle()
+    with pytest.raises(sbv.SBVError) as e:  # not prepared
+        h.predict(X[:10], 2, 10, y, theta)
+    assert e.value.code == 7
+    h = sbv.prepare(X, 10, 20, si.default_scale(3))
+    with pytest.raises(sbv.SBVError) as e:
+        h.predict(X[:10], 0, 10, y, theta)  # bs_pred < 1
+    assert e.value.code == 1
+    with pytest.raises(sbv.SBVError) as e:
+        h.predict(X[:10], 2, 2000, y, theta)  # m_pred beyond the grid kNN
+    assert e.value.code == 5
+    Xs = X[:10].copy()
+    Xs[2, 1] = np.inf
+    with pytest.raises(sbv.SBVError) as e:
+        h.predict(Xs, 2, 10, y, theta)
+    assert e.value.code == 1
+    with pytest.raises(sbv.SBVError) as e:
+        h.simulate(np.zeros(3), np.array([1.0, -0.5, 1.0]), 100, 1)  # negative variance
+    assert e.value.code == 1
+    with pytest.raises(sbv.SBVError) as e:
+        h.simulate(np.zeros(3), np.ones(3), 1, 1)  # n_sim < 2
+    assert e.value.code == 1
+
+
+def test_predict_general_nu(sbv, orc):
+    """N2 x N3: prediction through the K_nu covariance path."""
+    n, d = 2000, 3
+    X = si.make_X(n, d, seed=61)
+    y = si.make_y(X, seed=62)
+    Xs = si.make_X(300, d, seed=63)
+    sc = si.default_scale(d)
+    theta = si.default_theta(d, nu=1.2, tau2=1e-3)
+    h = sbv.prepare(X, 20, 40, sc)
+    check(h, orc, X, y, Xs, 5, 30, theta, sc)
