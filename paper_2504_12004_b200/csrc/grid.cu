@@ -443,6 +443,9 @@ cudaError_t launch_rac_grid(const double *S, int64_t n, int64_t i0, int d, const
 #define SBV_KNN_WARPS 4
 #endif
 constexpr int kKnnWarps = SBV_KNN_WARPS;
+// query counts up to ~one wave of one-warp queries (148 SMs x 6 CTAs x 4 warps
+// at 512-entry buffers) use the shared-query mode
+constexpr int64_t kKnnSplitQueries = 3000;
 constexpr int kKnnWcap = 1024;
 
 struct WCand {
@@ -561,7 +564,10 @@ __device__ void warp_select(const WCand *buf, int cnt, int m, int lane, unsigned
   thr_i = (int32_t)pre;
 }
 
-template <int DM>
+// QW warps per query (QW = 1: one warp per query; QW = kKnnWarps: the CTA's
+// warps split one query's candidates and meet at every ring end, for small
+// query counts where a single wave of one-warp queries is latency-bound).
+template <int DM, int QW>
 __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
     const double *__restrict__ Sperm, const int32_t *__restrict__ perm,
     const int64_t *__restrict__ off, const double *__restrict__ C,
@@ -570,9 +576,12 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
     int32_t *__restrict__ cnt_out, int wcap, const double *__restrict__ Cq, int32_t A_all) {
   extern __shared__ WCand sbuf[];  // kKnnWarps x wcap, then kKnnWarps x 256 histogram bins
   unsigned *hist = reinterpret_cast<unsigned *>(sbuf + kKnnWarps * wcap) + (threadIdx.x >> 5) * 256;
+  __shared__ double s_thr[2][kKnnWarps];  // QW > 1: per-warp m-th best at ring ends (by parity)
+  __shared__ int s_cnt[kKnnWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t li = blockIdx.x * (int64_t)kKnnWarps + w;
-  if (li >= k_local) return;
+  const int sub = w % QW;  // this warp's slice of the query
+  const int64_t li = blockIdx.x * (int64_t)(kKnnWarps / QW) + w / QW;
+  if (li >= k_local) return;  // QW > 1: one query per CTA, so the whole CTA returns
   WCand *buf = sbuf + w * wcap;
   // estimation: query = centroid of block t, admissible = strictly earlier
   // blocks [0, off_t); prediction (Cq): query = test centroid li, all n points
@@ -600,6 +609,7 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
   int count = 0;
   double thr_d = INFINITY;
   int32_t thr_i = INT32_MAX;
+  double gthr = INFINITY;  // QW > 1: min over the query's warps of their m-th best (a valid bound)
   int seen = 0;  // admissible points seen (for the "fewer than m exist" exit)
   // keep the m smallest keys (unsorted) and set the threshold to the m-th
   auto compact = [&]() {
@@ -630,7 +640,7 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
   // Short prefixes (the first blocks in zeta order) are scanned directly: the
   // grid would have to sweep most of the domain to find m sparse neighbours.
   if (A > 0 && m > 0 && A <= lv.direct_max) {
-    for (int base = 0; base < A; base += 32) {
+    for (int base = sub * 32; base < A; base += 32 * QW) {
       const int32_t pos = base + lane;
       const bool adm = pos < A;
       double acc = INFINITY;
@@ -670,7 +680,7 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
       int64_t box = side;
       if (G > 1) box *= side;
       if (G > 2) box *= side;
-      for (int64_t b0 = 0; b0 < box; b0 += 32) {
+      for (int64_t b0 = sub * 32; b0 < box; b0 += 32 * QW) {
         const int64_t bi = b0 + lane;
         int e_lo = 0, e_cnt = 0;
         if (bi < box) {
@@ -680,7 +690,7 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
           const int cc[3] = {q.cq[0] + o0, q.cq[1] + o1, q.cq[2] + o2};
           bool ok = max(abs(o0), max(abs(o1), abs(o2))) == r;
           for (int x = 0; x < G; x++) ok = ok && cc[x] >= 0 && cc[x] < g.nc[x];
-          if (ok && !(count >= m && !may_hold(cell_lb2(g, q, cc), thr_d))) {
+          if (ok && may_hold(cell_lb2(g, q, cc), fmin(count >= m ? thr_d : INFINITY, gthr))) {
             const int cell = cc[0] * g.stride[0] + (G > 1 ? cc[1] * g.stride[1] : 0) +
                              (G > 2 ? cc[2] * g.stride[2] : 0);
             const int s0 = c_start[cell], s1 = c_start[cell + 1];
@@ -730,7 +740,7 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
               }
             o = perm[pos];
           }
-          const bool ins = adm && wless(acc, o, thr_d, thr_i);
+          const bool ins = adm && wless(acc, o, thr_d, thr_i) && !(acc > gthr);
           const unsigned mask = __ballot_sync(0xffffffffu, ins);
           if (ins) {
             const int slot = count + __popc(mask & ((1u << lane) - 1));
@@ -743,15 +753,54 @@ __global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
         }
       }
       const double lb = ring_lb2(g, q, r);
-      if (lb < 0.0) break;
-      if (count >= m) {
-        // a full sort only when the threshold is unset or the buffer has
-        // grown well past m; otherwise test termination against the current
-        // (conservative) m-th best
-        if (thr_d == INFINITY || count > m + SBV_KNN_SLACK) compact();
-        if (!may_hold(lb, thr_d)) break;
+      if constexpr (QW == 1) {
+        if (lb < 0.0) break;
+        if (count >= m) {
+          // compact when the threshold is unset or the buffer has grown past
+          // m + slack; test termination against the current m-th best
+          if (thr_d == INFINITY || count > m + SBV_KNN_SLACK) compact();
+          if (!may_hold(lb, thr_d)) break;
+        }
+      } else {
+        // the query's warps agree on termination: the m-th best of the union
+        // is <= every warp's own m-th best, so their minimum bounds it
+        if (count > m || (count == m && thr_d == INFINITY)) compact();
+        if (lane == 0) s_thr[r & 1][w] = count >= m ? thr_d : INFINITY;
+        __syncthreads();
+        double gm = INFINITY;
+#pragma unroll
+        for (int x = 0; x < QW; x++) gm = fmin(gm, s_thr[r & 1][x]);
+        gthr = gm;
+        if (lb < 0.0) break;
+        if (gthr != INFINITY && !may_hold(lb, gthr)) break;
       }
     }
+  }
+  if constexpr (QW > 1) {
+    // merge the warps' candidates (each <= m after compaction) into warp 0's
+    // view of the CTA buffer, then select / sort as a single warp
+    compact();
+    if (lane == 0) s_cnt[w] = count;
+    __syncthreads();
+    if (sub != 0) return;
+    int total = 0;
+    for (int x = 0; x < QW; x++) {
+      const int cx = s_cnt[x];
+      const WCand *src = sbuf + x * wcap;
+      for (int base = 0; base < cx; base += 32) {  // forward copy, dst <= src
+        WCand e;
+        const bool has = base + lane < cx;
+        if (has) e = src[base + lane];
+        __syncwarp();
+        if (has) sbuf[total + base + lane] = e;
+        __syncwarp();
+      }
+      total += cx;
+    }
+    buf = sbuf;
+    count = total;
+    thr_d = INFINITY;
+    thr_i = INT32_MAX;
   }
   compact();
   warp_bitonic(buf, count, lane);  // the final m (or fewer) in (d2, orig) order
@@ -767,18 +816,31 @@ cudaError_t launch_knn_grid(const double *Sperm, const int32_t *perm, const int6
                             int32_t *nbr, int32_t *cnt, cudaStream_t st, const double *Cq, int32_t A_all) {
   if (k_local == 0) return cudaSuccess;
   if (m == 0) return cudaMemsetAsync(cnt, 0, k_local * 4, st);
-  const int grid = (int)((k_local + kKnnWarps - 1) / kKnnWarps);
+  // few queries (a fraction of one wave of one-warp queries): the CTA's warps
+  // share each query (SBV_KNN_QW overrides: 1 or 4)
+  int qw = k_local <= kKnnSplitQueries ? kKnnWarps : 1;
+  if (const char *e = getenv("SBV_KNN_QW")) qw = atoi(e) == kKnnWarps ? kKnnWarps : 1;
+  const int qpc = kKnnWarps / qw;  // queries per CTA
+  const int grid = (int)((k_local + qpc - 1) / qpc);
   const int thr = 32 * kKnnWarps;
-  // per-warp candidate buffer: the smallest power of two >= m + 160 (headroom
+  // per-warp candidate buffer: the smallest power of two >= m + 192 (headroom
   // between compactions) keeps shared memory low and occupancy high
   int wcap = SBV_KNN_WCAP;  // measured at cfg2: 256 / 512 / 1024 / 2048 -> 1.23 / 1.00 / 1.20 / 2.38 ms
   while (wcap < SBV_KNN_MINCAP(m)) wcap <<= 1;
   const int smem = (int)(sizeof(WCand) * kKnnWarps * wcap + sizeof(unsigned) * kKnnWarps * 256);
 #define SBV_KNN(DMv)                                                                                    \
   do {                                                                                                  \
-    cudaFuncSetAttribute(k_knn_grid<DMv>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);          \
-    k_knn_grid<DMv><<<grid, thr, smem, st>>>(Sperm, perm, off, C, local_blocks, k_local, d, m, lv,    \
-                                             c_start, c_list, nbr, cnt, wcap, Cq, A_all);              \
+    if (qw == 1) {                                                                                      \
+      cudaFuncSetAttribute(k_knn_grid<DMv, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);     \
+      k_knn_grid<DMv, 1><<<grid, thr, smem, st>>>(Sperm, perm, off, C, local_blocks, k_local, d, m, lv, \
+                                                  c_start, c_list, nbr, cnt, wcap, Cq, A_all);          \
+    } else {                                                                                            \
+      cudaFuncSetAttribute(k_knn_grid<DMv, kKnnWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                           smem);                                                                       \
+      k_knn_grid<DMv, kKnnWarps><<<grid, thr, smem, st>>>(Sperm, perm, off, C, local_blocks, k_local,   \
+                                                          d, m, lv, c_start, c_list, nbr, cnt, wcap,    \
+                                                          Cq, A_all);                                   \
+    }                                                                                                   \
   } while (0)
   if (d <= 4)
     SBV_KNN(4);

@@ -210,6 +210,21 @@ def test_grid_search_equals_brute_force(sbv, monkeypatch):
     assert hg.loglik(y, theta) == hb.loglik(y, theta)
 
 
+def test_knn_shared_query_mode_equals_warp_mode(sbv, monkeypatch):
+    """Few queries run with the CTA's warps sharing each query (SBV_KNN_QW=4);
+    the neighbour sets must equal the one-warp-per-query kernel's."""
+    import torch
+    n, d, bs, m = 200_000, 10, 100, 200
+    X = torch.from_numpy(si.make_X(n, d, seed=44)).cuda()
+    sc = si.default_scale(d)
+    monkeypatch.setenv("SBV_KNN_QW", "4")
+    h4 = sbv.prepare(X, bs, m, sc)
+    monkeypatch.setenv("SBV_KNN_QW", "1")
+    h1 = sbv.prepare(X, bs, m, sc)
+    for a, b in zip(h4.neighbors(), h1.neighbors()):
+        np.testing.assert_array_equal(a, b)
+
+
 def test_cfg2_full_size_sampled(sbv, orc):
     """BASELINE.json configs[1] (n=1e6, d=10, bs=100, m=200) in the launch
     configuration bench.py times: anchors, layout and centroids in full,
