@@ -443,9 +443,10 @@ cudaError_t launch_rac_grid(const double *S, int64_t n, int64_t i0, int d, const
 #define SBV_KNN_WARPS 4
 #endif
 constexpr int kKnnWarps = SBV_KNN_WARPS;
-// query counts up to ~one wave of one-warp queries (148 SMs x 6 CTAs x 4 warps
-// at 512-entry buffers) use the shared-query mode
-constexpr int64_t kKnnSplitQueries = 3000;
+// shared-query mode threshold: measured SLOWER at 2500 queries (4 GPUs, cfg2:
+// 0.47 vs 0.24 ms — the per-ring barriers and looser per-warp thresholds cost
+// more than the shorter chains gain), so it is off unless SBV_KNN_QW=4
+constexpr int64_t kKnnSplitQueries = 0;
 constexpr int kKnnWcap = 1024;
 
 struct WCand {
