@@ -137,7 +137,7 @@ def run_reference(args):
     oracle.build()
     c = workload(args.config)
     nthreads = os.cpu_count() or 1
-    n_s = args.ref_sample
+    n_s = args.ref_sample or 200_000
     for _ in range(args.warmup):
         oracle_sample(c, n_s, nthreads)
     times = []
@@ -380,7 +380,7 @@ def run_ours(args):
             import oracle
             oracle.build()
             nth = os.cpu_count() or 1
-            r = oracle_sample(c, args.ref_sample, nth)
+            r = oracle_sample(c, args.ref_sample or 400_000, nth)
             out["cpu_baseline"] = {"value": 1.0 / r["t_full"], "unit": "evals/s", "cores": nth,
                                    "kind": "oracle", "sample": r["sample"],
                                    "sample_seconds": r["t_prep"] + r["t_llh"]}
@@ -446,7 +446,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2")
-    ap.add_argument("--ref-sample", type=int, default=400_000)
+    ap.add_argument("--ref-sample", type=int, default=None,
+                    help="oracle sample size (default: 400k for the cpu_baseline leg, 200k per "
+                         "--impl reference step so K + W steps stay within a few minutes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-predict", action="store_true")
     args = ap.parse_args()
