@@ -373,6 +373,7 @@ int sbv_create(const sbv_opts *opts, sbv_handle *out) {
     h->profile = opts->profile;
   }
   for (int i = 0; i <= kMaxStages; i++) cudaEventCreate(&h->ev[i]);
+  cudaEventCreateWithFlags(&h->ev_sizes, cudaEventDisableTiming);
   if (cudaMallocHost(&h->result_host, 8 * sizeof(double)) != cudaSuccess ||
       cudaMallocHost(&h->flag_host, 2 * sizeof(int)) != cudaSuccess) {
     delete h;
@@ -396,6 +397,7 @@ void sbv_destroy(sbv_handle h) {
   if (h->comm) ncclCommDestroy(h->comm);
   for (int i = 0; i <= kMaxStages; i++)
     if (h->ev[i]) cudaEventDestroy(h->ev[i]);
+  if (h->ev_sizes) cudaEventDestroy(h->ev_sizes);
   if (h->result_host) cudaFreeHost(h->result_host);
   if (h->flag_host) cudaFreeHost(h->flag_host);
   if (h->pin) cudaFreeHost(h->pin);
@@ -538,6 +540,11 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   CU(ensure(h->local_blocks, h->k_local, unused));
   CU(cudaMemcpyAsync(h->local_blocks, local, h->k_local * sizeof(int32_t),
                      cudaMemcpyHostToDevice, st));
+  // block sizes to the host now: the launch geometry below needs only `off`
+  // (m_t = min(m, off_t) exactly: every admissible point is found when fewer
+  // than m exist), so the host works while the GPU runs H5-H6
+  CU(cudaMemcpyAsync(off_h, h->off, (k + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CU(cudaEventRecord(h->ev_sizes, st));
   CU(ensure(h->C, k * d, unused));
   CU(launch_centroids(h->Sperm, h->off, h->world > 1 ? h->local_blocks : nullptr, h->k_local, d,
                       h->C, st));
@@ -567,10 +574,9 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   CU(launch_gather_rows(Xd, h->perm, n, d, h->Xperm, st));
 
   // realised sizes -> LPT work order, statistics, H8 launch geometry
-  CU(cudaMemcpyAsync(off_h, h->off, (k + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  CU(cudaMemcpyAsync(cnt_h, h->cnt, h->k_local * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
+  CU(cudaEventSynchronize(h->ev_sizes));
   if (*h->flag_host) return fail(h, SBV_ERR_ARG, "X has non-finite entries");
+  for (int64_t li = 0; li < h->k_local; li++) cnt_h[li] = (int32_t)std::min<int64_t>(m, off_h[local[li]]);
   std::vector<int32_t> Nt(h->k_local);
   h->max_N = 0;
   h->min_bs = INT32_MAX;

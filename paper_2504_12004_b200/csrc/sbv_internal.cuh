@@ -87,6 +87,7 @@ struct Ctx {
   int *flag = nullptr;            // device: non-finite input flag
   int *flag_host = nullptr;       // pinned mirror
   char *pin = nullptr;            // pinned staging of prepare's host-side tables
+  cudaEvent_t ev_sizes = nullptr; // prepare: block offsets on the host
   size_t pin_cap = 0;
   unsigned int *queue = nullptr;  // work counter
   double *ws = nullptr;           // H8 per-CTA L workspaces
