@@ -56,12 +56,66 @@ __global__ void k_minmax_partial(const double *__restrict__ S, int64_t n, int d,
   }
 }
 
+// one pass over the rows (thread = row, coordinates in registers), then a
+// per-dimension warp / CTA reduction; d <= 16
+template <int DM>
+__global__ void __launch_bounds__(512) k_minmax_rows(const double *__restrict__ S, int64_t n, int d,
+                                                     double *part) {
+  __shared__ double smin[16][32], smax[16][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double lo[DM], hi[DM];
+#pragma unroll
+  for (int j = 0; j < DM; j++) {
+    lo[j] = INFINITY;
+    hi[j] = -INFINITY;
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int j = 0; j < DM; j++)
+      if (j < d) {
+        const double v = S[i * d + j];
+        lo[j] = fmin(lo[j], v);
+        hi[j] = fmax(hi[j], v);
+      }
+  }
+#pragma unroll
+  for (int j = 0; j < DM; j++) {
+    double a = lo[j], b = hi[j];
+    for (int o = 16; o > 0; o >>= 1) {
+      a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
+      b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    if (lane == 0) {
+      smin[j][w] = a;
+      smax[j][w] = b;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < d) {
+    const int j = threadIdx.x;
+    double a = INFINITY, b = -INFINITY;
+    for (int x = 0; x < (int)(blockDim.x >> 5); x++) {
+      a = fmin(a, smin[j][x]);
+      b = fmax(b, smax[j][x]);
+    }
+    part[(blockIdx.x * d + j) * 2] = a;
+    part[(blockIdx.x * d + j) * 2 + 1] = b;
+  }
+}
+
 cudaError_t data_extents(const double *S, int64_t n, int d, double *lo_hi_host, cudaStream_t st) {
   const int nb = 148;
   double *part = nullptr;
   cudaError_t e = cudaMallocAsync(&part, sizeof(double) * nb * d * 2, st);
   if (e) return e;
-  k_minmax_partial<<<nb, 1024, 0, st>>>(S, n, d, part);
+  if (d <= 4)
+    k_minmax_rows<4><<<nb, 512, 0, st>>>(S, n, d, part);
+  else if (d <= 8)
+    k_minmax_rows<8><<<nb, 512, 0, st>>>(S, n, d, part);
+  else if (d <= 16)
+    k_minmax_rows<16><<<nb, 512, 0, st>>>(S, n, d, part);
+  else
+    k_minmax_partial<<<nb, 1024, 0, st>>>(S, n, d, part);
   std::vector<double> h(nb * d * 2);
   e = cudaMemcpyAsync(h.data(), part, sizeof(double) * nb * d * 2, cudaMemcpyDeviceToHost, st);
   if (e) return e;
