@@ -464,6 +464,10 @@ cudaError_t launch_rac_grid(const double *S, int64_t n, int64_t i0, int d, const
     SBV_RAC(4);
   else if (d <= 8)
     SBV_RAC(8);
+  else if (d <= 10)
+    SBV_RAC(10);
+  else if (d <= 12)
+    SBV_RAC(12);
   else if (d <= 16)
     SBV_RAC(16);
   else if (d <= 32)
@@ -901,6 +905,10 @@ cudaError_t launch_knn_grid(const double *Sperm, const int32_t *perm, const int6
     SBV_KNN(4);
   else if (d <= 8)
     SBV_KNN(8);
+  else if (d <= 10)
+    SBV_KNN(10);
+  else if (d <= 12)
+    SBV_KNN(12);
   else if (d <= 16)
     SBV_KNN(16);
   else if (d <= 32)
