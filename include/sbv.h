@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SBV_ABI_VERSION 1
+#define SBV_ABI_VERSION 2
 #define SBV_MAX_D 64    /* 1 <= d <= 64 */
 
 typedef struct sbv_ctx *sbv_handle; /* opaque; owned by the library */
@@ -110,6 +110,18 @@ int sbv_prepare_ex(const double *X, int64_t n, int32_t d, int32_t bs, int32_t m,
 int sbv_prepare(const double *X, int64_t n, int32_t d, int32_t bs, int32_t m,
                 const double *scale, sbv_handle *out);
 
+/* Alg.1 with the block partition GIVEN (Alg.1 takes the block count K as an
+ * input; SURVEY 8(b) "block centroids given"): H2 (anchors) and H3 (RAC)
+ * are skipped and block_of_point[i] in [0, k) is point i's block, whose zeta
+ * position is its id (block 0 first).  H1 and H4-H6 run as in sbv_prepare_h
+ * (centroids = member means of the given blocks, kNN over strictly earlier
+ * blocks).  block_of_point: int32[n], host or device, read during the call.
+ * Errors: SBV_ERR_ARG (NULL, k outside [1, n], an id outside [0, k), an empty
+ * block, non-finite X / scale), otherwise as sbv_prepare_h.  sbv_get_anchors
+ * returns -1 for every block of such a handle. */
+int sbv_prepare_blocks(sbv_handle h, const double *X, int64_t n, int32_t d, int64_t k,
+                       const int32_t *block_of_point, int32_t m, const double *scale);
+
 /* ---------------------------------------------------------------- loglik */
 
 /* Alg.1 Steps 4-5: ell(theta; y) = sum_t ell_t with, per block t (Alg.5):
@@ -138,6 +150,29 @@ int sbv_loglik_parts(sbv_handle h, const double *y, const double *theta, double 
  * owned by other ranks are written as NaN.  quad/logdet may be NULL. */
 int sbv_block_terms(sbv_handle h, const double *y, const double *theta, double *terms,
                     double *quad, double *logdet);
+
+/* Exchange by the caller (SURVEY 8(b)'s alternative to sbv_comm_init, e.g.
+ * an MPI program, or one process driving several shards):
+ *  - sbv_set_shard(h, rank, world): shard this handle's blocks exactly as
+ *    sbv_comm_init would, without a communicator.  Must precede
+ *    sbv_prepare_h; prepare then runs RAC over all points on this device.
+ *    sbv_loglik on such a handle returns SBV_ERR_STATE.
+ *  - sbv_partials_size: number of doubles of one rank's partials
+ *    (= 8 x ceil(chunks / world); chunk = 64 zeta-consecutive blocks).
+ *  - sbv_loglik_partials: Steps 4 and 5's per-rank part (H7-H9): this rank's
+ *    chunk partial sums {sum ell_t, sum quad, sum logdet, #points, #failed,
+ *    lowest failing block, its stage, 0} per local chunk, in the slot layout
+ *    of the allgather (host or device buffer of sbv_partials_size doubles).
+ *  - sbv_reduce_partials: Step 5: all ranks' partials concatenated
+ *    in rank order (world x sbv_partials_size doubles, host or device) are
+ *    summed in global chunk order with the fixed tree of sbv_loglik, so the
+ *    result is bit-identical to a one-GPU sbv_loglik.  parts: host
+ *    double[4] = {ell, sum quad, sum logdet, #points}.  Errors as sbv_loglik
+ *    (SBV_ERR_NOT_PD with the lowest failing block in sbv_last_error). */
+int sbv_set_shard(sbv_handle h, int32_t rank, int32_t world);
+int sbv_partials_size(sbv_handle h, int64_t *count);
+int sbv_loglik_partials(sbv_handle h, const double *y, const double *theta, double *partials);
+int sbv_reduce_partials(sbv_handle h, const double *all_partials, double *parts);
 
 /* ---------------------------------------------------------------- introspection */
 

@@ -1,5 +1,7 @@
 // h8_host.cu — host side of H8 (h8_kernel.cuh): workspace / shared-memory
 // sizing, occupancy, variant selection and launch.
+#include <stdio.h>
+
 #include "h8_kernel.cuh"
 
 namespace sbv {
@@ -109,7 +111,37 @@ cudaError_t launch_h8_problem(const H8Problem &pb, int d, const double *theta, u
   if (pb.k_local == 0) return cudaSuccess;
   const H8Fn f = pick(nu, d, pb.predict);
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pb.smem);
+  a.trace = nullptr;
+  a.trace_n = nullptr;
+  a.trace_cap = 0;
+#if SBV_TRACE  // tool-only build (tools/h8_trace.py): per-task timeline of this launch
+  static unsigned long long *tbuf = nullptr;
+  static unsigned int *tn = nullptr;
+  const unsigned int cap = 4u << 20;
+  if (!tbuf) {
+    cudaMalloc(&tbuf, (size_t)cap * 6 * sizeof(unsigned long long));
+    cudaMalloc(&tn, sizeof(unsigned int));
+  }
+  cudaMemsetAsync(tn, 0, sizeof(unsigned int), st);
+  a.trace = tbuf;
+  a.trace_n = tn;
+  a.trace_cap = cap;
+#endif
   f<<<pb.grid, kH8Threads, pb.smem, st>>>(a);
+#if SBV_TRACE
+  if (const char *out = getenv("SBV_TRACE_OUT")) {
+    unsigned int n = 0;
+    cudaMemcpyAsync(&n, tn, sizeof(n), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    n = n < cap ? n : cap;
+    std::vector<unsigned long long> h((size_t)n * 6);
+    cudaMemcpy(h.data(), tbuf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    if (FILE *fp = fopen(out, "wb")) {
+      fwrite(h.data(), sizeof(unsigned long long), h.size(), fp);
+      fclose(fp);
+    }
+  }
+#endif
   return cudaGetLastError();
 }
 

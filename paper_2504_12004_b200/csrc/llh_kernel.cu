@@ -13,14 +13,15 @@
 // [y'_J ; v] with v = L'^{-1}(y_B - mu_cor) (TRSV + GEMV + TRSV).  So
 // ell_t = -1/2 (sum_{j in B} v_j^2 + 2 sum_{j in B} log L_jj) - bs_t/2 log 2pi.
 //
-// Factorisation: left-looking in 32-column panels.  For panel j the rows
-// [32j, N] are (re)generated from the Matérn closed form (Eq.5-6) straight
-// into DMMA accumulators, updated by -L[rows, 0:32j] L[panel, 0:32j]^T with
-// FP64 tensor-core mma.sync m8n8k4 (SASS DMMA.8x8x4), the 32x32 diagonal
-// tile is factored in shared memory and the rows below are solved against
-// it.  Finished panels go to a per-CTA L workspace in global memory (L2
-// resident) stored in 8x4 "fragment micro-tiles" so that every DMMA operand
-// fragment is one coalesced 256-byte warp load.
+// Factorisation (h8_kernel.cuh): left-looking in 32-column panels.  For panel
+// j the rows [32j, N] are generated from the Matérn closed form (Eq.5-6) into
+// the panel's workspace slot, loaded into DMMA accumulators and updated by
+// -L[rows, 0:32j] L[panel, 0:32j]^T with FP64 tensor-core mma.sync m8n8k4
+// (SASS DMMA.8x8x4); the 32x32 diagonal tile is factored in shared memory and
+// the rows below are solved against it.  Finished panels go to a per-CTA L
+// workspace in global memory (L2 resident) stored in 8x4 "fragment
+// micro-tiles" so that every DMMA operand fragment is one coalesced 256-byte
+// warp load.
 #include <math.h>
 
 #include "sbv_internal.cuh"

@@ -292,9 +292,14 @@ int validate_theta(sbv_ctx *h, const double *theta) {
 
 // Steps 4-5 for the current handle; leaves per-block outputs on device and
 // the reduced vector in h->result_host.
-int run_loglik(sbv_ctx *h, const double *y, const double *theta) {
+// partials != nullptr: stop after H9 and copy this rank's chunk partials
+// (sbv_loglik_partials); otherwise the full H7-H10 path.
+int run_loglik(sbv_ctx *h, const double *y, const double *theta, double *partials = nullptr) {
   if (!h->prepared) return fail(h, SBV_ERR_STATE, "sbv_loglik before sbv_prepare");
   if (!y) return fail(h, SBV_ERR_ARG, "y is NULL");
+  if (!partials && h->world > 1 && !h->comm)
+    return fail(h, SBV_ERR_STATE, "sharded without a communicator (sbv_set_shard): use "
+                                  "sbv_loglik_partials + sbv_reduce_partials");
   int rc = validate_theta(h, theta);
   if (rc) return rc;
   CU(cudaSetDevice(h->device));
@@ -311,9 +316,15 @@ int run_loglik(sbv_ctx *h, const double *y, const double *theta) {
   tm.mark("H8_block_llh");
   CU(launch_reduce_chunks(*h, h->stream));
   tm.mark("H9_chunk_sums");
+  if (partials) {
+    CU(cudaMemcpyAsync(partials, h->chunk_local, (size_t)h->ncl_pad * 8 * sizeof(double),
+                       cudaMemcpyDefault, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    tm.finish();
+    return SBV_OK;
+  }
   if (h->world > 1) {
-    int64_t ncl_pad = (h->n_chunks + h->world - 1) / h->world;
-    NC(ncclAllGather(h->chunk_local, h->chunk_all, (size_t)ncl_pad * 8, ncclDouble, h->comm,
+    NC(ncclAllGather(h->chunk_local, h->chunk_all, (size_t)h->ncl_pad * 8, ncclDouble, h->comm,
                      h->stream));
     tm.mark("H10_allgather");
   }
@@ -374,9 +385,11 @@ int sbv_create(const sbv_opts *opts, sbv_handle *out) {
   }
   for (int i = 0; i <= kMaxStages; i++) cudaEventCreate(&h->ev[i]);
   cudaEventCreateWithFlags(&h->ev_sizes, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&h->ev_pin, cudaEventDisableTiming);
   if (cudaMallocHost(&h->result_host, 8 * sizeof(double)) != cudaSuccess ||
       cudaMallocHost(&h->flag_host, 2 * sizeof(int)) != cudaSuccess) {
-    delete h;
+    cudaGetLastError();
+    sbv_destroy(h);  // frees whatever was created (events, pinned buffers)
     return SBV_ERR_OOM;
   }
   // keep stream-ordered temporaries (CUB sort scratch) pooled across calls
@@ -398,6 +411,7 @@ void sbv_destroy(sbv_handle h) {
   for (int i = 0; i <= kMaxStages; i++)
     if (h->ev[i]) cudaEventDestroy(h->ev[i]);
   if (h->ev_sizes) cudaEventDestroy(h->ev_sizes);
+  if (h->ev_pin) cudaEventDestroy(h->ev_pin);
   if (h->result_host) cudaFreeHost(h->result_host);
   if (h->flag_host) cudaFreeHost(h->flag_host);
   if (h->pin) cudaFreeHost(h->pin);
@@ -431,33 +445,55 @@ int sbv_comm_init(sbv_handle h, const void *nccl_unique_id, int32_t rank, int32_
   return SBV_OK;
 }
 
-int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t bs, int32_t m,
-                  const double *scale) {
+}  // extern "C"
+
+namespace {
+
+__global__ void k_check_blocks(const int32_t *bo, int64_t n, int64_t k, int *bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (bo[i] < 0 || bo[i] >= k) *bad = 1;
+}
+
+// Alg.1 Steps 1-3.  given_bo == nullptr: H2 anchors + H3 RAC define the
+// blocks (k = round(n/bs)); otherwise the caller's partition (block id = zeta
+// position, k = kk blocks) replaces H2/H3 ("block centroids given").
+int prepare_impl(sbv_ctx *h, const double *X, int64_t n, int32_t d, int32_t bs, int32_t m,
+                 const double *scale, const int32_t *given_bo, int64_t kk) {
   if (!h) return SBV_ERR_ARG;
   if (!X || !scale) return fail(h, SBV_ERR_ARG, "X or scale is NULL");
   if (n < 1 || n >= (int64_t(1) << 31)) return fail(h, SBV_ERR_ARG, "n out of range");
   if (d < 1 || d > SBV_MAX_D) return fail(h, SBV_ERR_ARG, "d out of range [1, 64]");
-  if (bs < 1 || bs > n) return fail(h, SBV_ERR_ARG, "bs out of range [1, n]");
+  if (given_bo) {
+    if (kk < 1 || kk > n) return fail(h, SBV_ERR_ARG, "block count out of range [1, n]");
+  } else if (bs < 1 || bs > n) {
+    return fail(h, SBV_ERR_ARG, "bs out of range [1, n]");
+  }
   if (m < 0) return fail(h, SBV_ERR_ARG, "m must be >= 0");
   if (m > 1536) return fail(h, SBV_ERR_UNSUPPORTED, "m > 1536 not supported by the kNN kernel");
   for (int j = 0; j < d; j++)
     if (!(scale[j] > 0) || !isfinite(scale[j])) return fail(h, SBV_ERR_ARG, "scale_j must be finite and > 0");
   CU(cudaSetDevice(h->device));
+  // the previous prepare's async H2D copies out of the pinned staging must be
+  // done before the staging is rewritten below
+  CU(cudaEventSynchronize(h->ev_pin));
   h->prepared = false;
   h->lv_valid = false;
   h->ks = 0;
   h->n = n;
   h->d = d;
-  h->bs = bs;
+  h->bs = given_bo ? (int32_t)std::max<int64_t>(1, n / kk) : bs;
   h->m = m;
+  h->given_blocks = given_bo ? 1 : 0;
   h->scale.assign(scale, scale + d);
-  const int64_t k = std::max<int64_t>(1, (2 * n + bs) / (2 * (int64_t)bs));  // round(n/bs)
+  const int64_t k = given_bo ? kk : std::max<int64_t>(1, (2 * n + bs) / (2 * (int64_t)bs));  // round(n/bs)
   h->k = k;
   cudaStream_t st = h->stream;
   auto &unused = h->cap;
   Timer tm(h, 1);
 
-  // device inputs are read in place (valid for the duration of the call);
+  // device inputs are read in place (valid for the duration of the call:
+  // every kernel reading X is queued before the host wait on ev_sizes below);
   // host inputs are staged once
   const double *Xd = X;
   if (!is_device_ptr(X)) {
@@ -465,34 +501,44 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
     CU(cudaMemcpyAsync(h->X, X, n * d * sizeof(double), cudaMemcpyDefault, st));
     Xd = h->X;
   }
-  // finiteness flag: read back at the first host sync below (no extra stall)
-  CU(ensure(h->flag, 2, unused));
-  CU(cudaMemsetAsync(h->flag, 0, sizeof(int), st));
-  k_check_finite<<<grid_for(n * d), 256, 0, st>>>(Xd, n * d, h->flag);
-  CU(cudaMemcpyAsync(h->flag_host, h->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   tm.mark("h2d_X");
   CU(ensure(h->S, n * d, unused));
   CU(launch_scale(Xd, n, d, scale, h->S, st));
+  // finiteness of S = X / scale (a finite X over a tiny scale can overflow);
+  // the flag is read back at the first host sync below (no extra stall)
+  CU(ensure(h->flag, 2, unused));
+  CU(cudaMemsetAsync(h->flag, 0, 2 * sizeof(int), st));
+  k_check_finite<<<grid_for(n * d), 256, 0, st>>>(h->S, n * d, h->flag);
   tm.mark("H1_scale");
   CU(ensure(h->anchors, k, unused));
-  if (h->use_grid) {  // filtered selection; verified at the next host sync (extents)
+  CU(ensure(h->block_of, n, unused));
+  if (given_bo) {
+    k_fill_i<<<grid_for(k), 256, 0, st>>>(h->anchors, k, -1);  // no anchors: partition given
+    CU(cudaMemcpyAsync(h->block_of, given_bo, n * sizeof(int32_t), cudaMemcpyDefault, st));
+    k_check_blocks<<<grid_for(n), 256, 0, st>>>(h->block_of, n, k, h->flag);
+  } else if (h->use_grid) {  // filtered selection; verified at the next host sync (extents)
     CU(select_anchors_fast(n, k, h->seed, h->anchors, h->flag + 1, st));
-    CU(cudaMemcpyAsync(h->flag_host + 1, h->flag + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
   } else {
     CU(select_anchors(n, k, h->seed, h->anchors, nullptr, 0, st, nullptr));
   }
-  tm.mark("H2_anchors");
-  CU(ensure(h->block_of, n, unused));
+  CU(cudaMemcpyAsync(h->flag_host, h->flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  tm.mark(given_bo ? "H2_given_blocks" : "H2_anchors");
   double lo_hi[2 * SBV_MAX_D];
   if (h->use_grid) {
     CU(data_extents(h->S, n, d, lo_hi, st));  // one small D2H (grid geometry) + sync
-    if (h->flag_host[1] != 0) CU(select_anchors(n, k, h->seed, h->anchors, nullptr, 0, st, nullptr));
+    if (*h->flag_host) return fail(h, SBV_ERR_ARG, given_bo ? "X/scale non-finite or block id out of [0, k)"
+                                                             : "X has non-finite entries (or X/scale overflows)");
+    if (!given_bo && h->flag_host[1] != 0) CU(select_anchors(n, k, h->seed, h->anchors, nullptr, 0, st, nullptr));
     tm.mark("extents");
+  }
+  if (given_bo) {
+    // H3 skipped
+  } else if (h->use_grid) {
     const GridDesc ga = make_grid(lo_hi, d, k, 3.0);
     CU(ensure(h->a_start, ga.ncells + 1, unused));
     CU(ensure(h->a_list, k, unused));
     CU(build_cells(h->S, h->anchors, k, d, ga, h->a_start, h->a_list, st));
-    if (h->world > 1) {
+    if (h->world > 1 && h->comm) {
       // RAC sharded by points: rank r assigns points [r c, (r+1) c), then one
       // in-place allgather rebuilds block_of everywhere (NVLink, 4 B/point)
       const int64_t chunk = (n + h->world - 1) / h->world;
@@ -514,6 +560,10 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   CU(build_layout(h->block_of, n, k, h->perm, h->off, nullptr, 0, st, nullptr));
   CU(ensure(h->Sperm, n * d, unused));
   CU(launch_gather_rows(h->S, h->perm, n, d, h->Sperm, st));
+  // block-major ORIGINAL inputs for H8: the last read of the caller's X, queued
+  // before the ev_sizes host wait, so X may be freed when prepare returns
+  CU(ensure(h->Xperm, n * d, unused));
+  CU(launch_gather_rows(Xd, h->perm, n, d, h->Xperm, st));
   tm.mark("H4_layout");
   // shard: 64-block chunks of zeta order dealt round-robin over ranks
   h->n_chunks = (k + kChunkBlocks - 1) / kChunkBlocks;
@@ -542,9 +592,17 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
                      cudaMemcpyHostToDevice, st));
   // block sizes to the host now: the launch geometry below needs only `off`
   // (m_t = min(m, off_t) exactly: every admissible point is found when fewer
-  // than m exist), so the host works while the GPU runs H5-H6
+  // than m exist, all distances being finite), so the host works while the
+  // GPU runs H5-H6
   CU(cudaMemcpyAsync(off_h, h->off, (k + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(h->flag_host, h->flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
   CU(cudaEventRecord(h->ev_sizes, st));
+  if (given_bo) {  // a caller partition is validated before H5-H6 run on it
+    CU(cudaEventSynchronize(h->ev_sizes));
+    if (*h->flag_host) return fail(h, SBV_ERR_ARG, "X/scale non-finite or block id out of [0, k)");
+    for (int64_t t = 0; t < k; t++)
+      if (off_h[t + 1] == off_h[t]) return fail(h, SBV_ERR_ARG, "given partition has an empty block");
+  }
   CU(ensure(h->C, k * d, unused));
   CU(launch_centroids(h->Sperm, h->off, h->world > 1 ? h->local_blocks : nullptr, h->k_local, d,
                       h->C, st));
@@ -569,13 +627,11 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   }
   tm.mark("H6_knn");
 
-  // block-major original inputs for H8 (queued before the host sync below)
-  CU(ensure(h->Xperm, n * d, unused));
-  CU(launch_gather_rows(Xd, h->perm, n, d, h->Xperm, st));
-
   // realised sizes -> LPT work order, statistics, H8 launch geometry
   CU(cudaEventSynchronize(h->ev_sizes));
-  if (*h->flag_host) return fail(h, SBV_ERR_ARG, "X has non-finite entries");
+  if (*h->flag_host)
+    return fail(h, SBV_ERR_ARG, given_bo ? "X/scale non-finite or block id out of [0, k)"
+                                         : "X has non-finite entries (or X/scale overflows)");
   for (int64_t li = 0; li < h->k_local; li++) cnt_h[li] = (int32_t)std::min<int64_t>(m, off_h[local[li]]);
   std::vector<int32_t> Nt(h->k_local);
   h->max_N = 0;
@@ -595,7 +651,7 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
     h->entries += mt * (mt + 1) / 2 + mt * b + b * (b + 1) / 2;
     h->knn_pairs += (double)off_h[t];
   }
-  h->rac_pairs = (double)n * (double)k;
+  h->rac_pairs = given_bo ? 0.0 : (double)n * (double)k;
   h->h8_bytes = 0;
   for (int64_t li = 0; li < h->k_local; li++)
     h->h8_bytes += (double)Nt[li] * (d + 1) * 8.0 + (double)cnt_h[li] * 4.0 + 4 * 8.0;
@@ -609,6 +665,7 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   CU(ensure(h->work_order, h->k_local, unused));
   CU(cudaMemcpyAsync(h->work_order, order, h->k_local * sizeof(int32_t),
                      cudaMemcpyHostToDevice, st));
+  CU(cudaEventRecord(h->ev_pin, st));  // the next prepare waits on it before reusing `pin`
 
   // per-eval buffers
   CU(ensure(h->yperm, n, unused));
@@ -618,6 +675,7 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   CU(ensure(h->logdets, h->k_local, unused));
   CU(ensure(h->status, h->k_local, unused));
   const int64_t ncl_pad = h->world > 1 ? (h->n_chunks + h->world - 1) / h->world : h->n_chunks;
+  h->ncl_pad = ncl_pad;
   CU(ensure(h->chunk_local, std::max<int64_t>(ncl_pad, 1) * 8, unused));
   CU(cudaMemsetAsync(h->chunk_local, 0, std::max<int64_t>(ncl_pad, 1) * 8 * sizeof(double), st));
   if (h->world > 1) CU(ensure(h->chunk_all, (int64_t)h->world * ncl_pad * 8, unused));
@@ -642,12 +700,27 @@ int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t b
   h->ws_per_cta = h8_ws_doubles(std::max(h->max_N, 1), d);
   CU(ensure(h->ws, (size_t)h->h8_grid * h->ws_per_cta, unused));
   // no trailing host sync: everything above is stream-ordered before the
-  // first sbv_loglik, and the pinned staging is only rewritten after the next
-  // prepare's own first sync
+  // first sbv_loglik; the pinned staging is guarded by ev_pin
   tm.mark("meta");
   tm.finish();
   h->prepared = true;
   return SBV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sbv_prepare_h(sbv_handle h, const double *X, int64_t n, int32_t d, int32_t bs, int32_t m,
+                  const double *scale) {
+  return prepare_impl(h, X, n, d, bs, m, scale, nullptr, 0);
+}
+
+int sbv_prepare_blocks(sbv_handle h, const double *X, int64_t n, int32_t d, int64_t k,
+                       const int32_t *block_of_point, int32_t m, const double *scale) {
+  if (!h) return SBV_ERR_ARG;
+  if (!block_of_point) return fail(h, SBV_ERR_ARG, "block_of_point is NULL");
+  return prepare_impl(h, X, n, d, 1, m, scale, block_of_point, k);
 }
 
 int sbv_prepare_ex(const double *X, int64_t n, int32_t d, int32_t bs, int32_t m,
@@ -674,8 +747,6 @@ int sbv_prepare(const double *X, int64_t n, int32_t d, int32_t bs, int32_t m, co
 int sbv_loglik_parts(sbv_handle h, const double *y, const double *theta, double *parts) {
   if (!h) return SBV_ERR_ARG;
   int rc = run_loglik(h, y, theta);
-  const double two_pi_half = 0.91893853320467274178;  // log(2 pi) / 2
-  (void)two_pi_half;
   if (parts) {
     parts[0] = rc == SBV_OK ? h->result_host[0] : NAN;
     parts[1] = h->result_host[1];
@@ -683,6 +754,59 @@ int sbv_loglik_parts(sbv_handle h, const double *y, const double *theta, double 
     parts[3] = h->result_host[3];
   }
   return rc;
+}
+
+int sbv_set_shard(sbv_handle h, int32_t rank, int32_t world) {
+  if (!h || world < 1 || rank < 0 || rank >= world) return SBV_ERR_ARG;
+  if (h->prepared) return fail(h, SBV_ERR_STATE, "sbv_set_shard must precede sbv_prepare_h");
+  if (h->comm) {
+    ncclCommDestroy(h->comm);
+    h->comm = nullptr;
+  }
+  h->rank = rank;
+  h->world = world;
+  return SBV_OK;
+}
+
+int sbv_partials_size(sbv_handle h, int64_t *count) {
+  if (!h || !count) return SBV_ERR_ARG;
+  if (!h->prepared) return fail(h, SBV_ERR_STATE, "not prepared");
+  *count = h->ncl_pad * 8;
+  return SBV_OK;
+}
+
+int sbv_loglik_partials(sbv_handle h, const double *y, const double *theta, double *partials) {
+  if (!h) return SBV_ERR_ARG;
+  if (!partials) return fail(h, SBV_ERR_ARG, "partials is NULL");
+  return run_loglik(h, y, theta, partials);
+}
+
+int sbv_reduce_partials(sbv_handle h, const double *all_partials, double *parts) {
+  if (!h) return SBV_ERR_ARG;
+  if (!h->prepared) return fail(h, SBV_ERR_STATE, "not prepared");
+  if (!all_partials || !parts) return fail(h, SBV_ERR_ARG, "NULL argument");
+  CU(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  const size_t cnt = (size_t)h->world * h->ncl_pad * 8;
+  double *dst = h->chunk_local;
+  if (h->world > 1) {
+    CU(ensure(h->chunk_all, (int64_t)cnt, h->cap));
+    dst = h->chunk_all;
+  }
+  CU(cudaMemcpyAsync(dst, all_partials, cnt * sizeof(double), cudaMemcpyDefault, st));
+  CU(launch_final_reduce(*h, st));
+  CU(cudaMemcpyAsync(h->result_host, h->result, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  parts[0] = h->result_host[4] > 0 ? NAN : h->result_host[0];
+  parts[1] = h->result_host[1];
+  parts[2] = h->result_host[2];
+  parts[3] = h->result_host[3];
+  if (h->result_host[4] > 0) {
+    h->err_block = (int64_t)h->result_host[5];
+    h->err_stage = (int32_t)h->result_host[6];
+    return fail(h, SBV_ERR_NOT_PD, "Cholesky factorisation failed (non-positive pivot)");
+  }
+  return SBV_OK;
 }
 
 int sbv_loglik(sbv_handle h, const double *y, const double *theta, double *ll) {
@@ -696,7 +820,9 @@ int sbv_loglik(sbv_handle h, const double *y, const double *theta, double *ll) {
 int sbv_block_terms(sbv_handle h, const double *y, const double *theta, double *terms,
                     double *quad, double *logdet) {
   if (!h) return SBV_ERR_ARG;
-  int rc = run_loglik(h, y, theta);
+  std::vector<double> part;  // sharded without a communicator: stop after H9
+  if (h->prepared && h->world > 1 && !h->comm) part.resize((size_t)h->ncl_pad * 8 + 1);
+  int rc = run_loglik(h, y, theta, part.empty() ? nullptr : part.data());
   if (rc != SBV_OK && rc != SBV_ERR_NOT_PD) return rc;
   double *tmp = nullptr;
   cudaStream_t st = h->stream;
@@ -708,7 +834,10 @@ int sbv_block_terms(sbv_handle h, const double *y, const double *theta, double *
     k_fill_d<<<grid_for(h->k), 256, 0, st>>>(tmp, h->k, NAN);
     k_scatter_terms<<<grid_for(h->k_local), 256, 0, st>>>(srcs[i], h->local_blocks, h->k_local, tmp);
     int r2 = copy_out(h, dsts[i], tmp, h->k * sizeof(double));
-    if (r2) return r2;
+    if (r2) {
+      cudaFreeAsync(tmp, st);
+      return r2;
+    }
   }
   cudaFreeAsync(tmp, st);
   CU(cudaStreamSynchronize(st));
@@ -982,10 +1111,11 @@ int sbv_get_prediction(sbv_handle h, int64_t *ks, int32_t *anchors, int32_t *blo
     CU(cudaMallocAsync(&tc, h->ks * sizeof(int32_t), st));
     k_nbr_to_orig<<<grid_for(std::max<int64_t>(h->ks * mp, h->ks)), 256, 0, st>>>(
         h->q_nbr, h->q_cnt, h->perm, h->q_local, h->ks, mp, tn, tc);
-    if ((rc = copy_out(h, nbr, tn, h->ks * mp * sizeof(int32_t)))) return rc;
-    if ((rc = copy_out(h, cnt, tc, h->ks * sizeof(int32_t)))) return rc;
+    rc = copy_out(h, nbr, tn, h->ks * mp * sizeof(int32_t));
+    if (!rc) rc = copy_out(h, cnt, tc, h->ks * sizeof(int32_t));
     cudaFreeAsync(tn, st);
     cudaFreeAsync(tc, st);
+    if (rc) return rc;
   }
   return SBV_OK;
 }

@@ -69,6 +69,7 @@ struct Ctx {
   int32_t *work_order = nullptr;   // k_local indices into local_blocks, LPT order
   int64_t k_local = 0;
   int64_t n_chunks = 0, n_chunks_local = 0;
+  int64_t ncl_pad = 0;  // chunk-partial slots per rank (allgather layout)
   int32_t max_N = 0, min_bs = 0, max_bs = 0;
   double flops = 0, entries = 0, knn_pairs = 0, rac_pairs = 0, h8_bytes = 0;
   // per-eval buffers
@@ -88,6 +89,8 @@ struct Ctx {
   int *flag_host = nullptr;       // pinned mirror
   char *pin = nullptr;            // pinned staging of prepare's host-side tables
   cudaEvent_t ev_sizes = nullptr; // prepare: block offsets on the host
+  cudaEvent_t ev_pin = nullptr;   // prepare: last async H2D copy out of the pinned staging
+  int given_blocks = 0;           // 1: the caller supplied the block partition (no H2/H3)
   size_t pin_cap = 0;
   unsigned int *queue = nullptr;  // work counter
   double *ws = nullptr;           // H8 per-CTA L workspaces

@@ -40,10 +40,12 @@ _lib = None
 
 EXPORTS = ["sbv_abi_version", "sbv_create", "sbv_destroy", "sbv_comm_unique_id", "sbv_comm_init",
            "sbv_shard_blocks",
-           "sbv_prepare_h", "sbv_prepare_ex", "sbv_prepare", "sbv_loglik", "sbv_loglik_parts",
+           "sbv_prepare_h", "sbv_prepare_ex", "sbv_prepare", "sbv_prepare_blocks", "sbv_loglik",
+           "sbv_loglik_parts",
            "sbv_block_terms", "sbv_num_blocks", "sbv_get_anchors", "sbv_get_blocks",
            "sbv_get_neighbors", "sbv_stats", "sbv_stage_times", "sbv_last_error",
-           "sbv_predict", "sbv_get_prediction", "sbv_simulate"]
+           "sbv_predict", "sbv_get_prediction", "sbv_simulate", "sbv_set_shard",
+           "sbv_partials_size", "sbv_loglik_partials", "sbv_reduce_partials"]
 
 
 def lib():
@@ -64,6 +66,11 @@ def lib():
         L.sbv_prepare_ex.argtypes = [_p, _i64, _i32, _i32, _i32, _p, ctypes.POINTER(sbv_opts),
                                      ctypes.POINTER(_p)]
         L.sbv_prepare.argtypes = [_p, _i64, _i32, _i32, _i32, _p, ctypes.POINTER(_p)]
+        L.sbv_set_shard.argtypes = [_p, _i32, _i32]
+        L.sbv_partials_size.argtypes = [_p, ctypes.POINTER(_i64)]
+        L.sbv_loglik_partials.argtypes = [_p, _p, _p, _p]
+        L.sbv_reduce_partials.argtypes = [_p, _p, _p]
+        L.sbv_prepare_blocks.argtypes = [_p, _p, _i64, _i32, _i64, _p, _i32, _p]
         L.sbv_loglik.argtypes = [_p, _p, _p, ctypes.POINTER(ctypes.c_double)]
         L.sbv_loglik_parts.argtypes = [_p, _p, _p, _p]
         L.sbv_block_terms.argtypes = [_p, _p, _p, _p, _p, _p]
@@ -154,6 +161,27 @@ class Handle:
         buf = ctypes.create_string_buffer(unique_id, 128)
         self._check(lib().sbv_comm_init(self._h, buf, rank, world))
 
+    def set_shard(self, rank: int, world: int):
+        """sbv_set_shard: shard without a communicator (caller-side exchange)."""
+        self._check(lib().sbv_set_shard(self._h, rank, world))
+
+    def loglik_partials(self, y, theta):
+        y = _f64(y)
+        th = np.ascontiguousarray(theta, dtype=np.float64)
+        py, _k = _ptr(y)
+        cnt = _i64(0)
+        rc = lib().sbv_partials_size(self._h, ctypes.byref(cnt))
+        self._check(rc)
+        out = np.zeros(cnt.value)
+        self._check(lib().sbv_loglik_partials(self._h, py, th.ctypes.data_as(_p), out.ctypes.data_as(_p)))
+        return out
+
+    def reduce_partials(self, all_partials):
+        a = np.ascontiguousarray(all_partials, dtype=np.float64)
+        parts = np.zeros(4)
+        self._check(lib().sbv_reduce_partials(self._h, a.ctypes.data_as(_p), parts.ctypes.data_as(_p)))
+        return parts
+
     def prepare(self, X, bs: int, m: int, scale):
         X = _f64(X)
         n, d = X.shape
@@ -163,6 +191,26 @@ class Handle:
         px, _k = _ptr(X)
         self._check(lib().sbv_prepare_h(self._h, px, n, d, bs, m, sc.ctypes.data_as(_p)))
         self.n, self.d, self.bs, self.m = n, d, bs, m
+        return self
+
+    def prepare_blocks(self, X, block_of, m: int, scale, k: int = None):
+        """sbv_prepare_blocks: the block partition is given (block id = zeta position)."""
+        X = _f64(X)
+        n, d = X.shape
+        sc = np.ascontiguousarray(scale, dtype=np.float64)
+        if sc.shape != (d,):
+            raise SBVError(SBV_ERR_ARG, "scale must have length d")
+        if hasattr(block_of, "data_ptr"):
+            bo = block_of.contiguous()
+            pb = bo.data_ptr()
+            kk = int(bo.max().item()) + 1 if k is None else k
+        else:
+            bo = np.ascontiguousarray(block_of, dtype=np.int32)
+            pb = bo.ctypes.data
+            kk = int(bo.max()) + 1 if k is None else k
+        px, _k = _ptr(X)
+        self._check(lib().sbv_prepare_blocks(self._h, px, n, d, kk, _p(pb), m, sc.ctypes.data_as(_p)))
+        self.n, self.d, self.bs, self.m = n, d, max(1, n // kk), m
         return self
 
     def destroy(self):

@@ -40,7 +40,7 @@ def test_binding_lists_every_export():
 
 
 def test_abi_version(libsbv):
-    assert libsbv.sbv_abi_version() == 1
+    assert libsbv.sbv_abi_version() == 2
 
 
 def test_library_is_sm100a_and_uses_dmma(libsbv):

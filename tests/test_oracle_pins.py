@@ -368,3 +368,59 @@ def test_rac_random_is_nearest_anchor(orc):
         dd = _np_d2(S[i], S[anc])
         got = P["block_of"][i]
         assert dd[got] <= dd.min() * (1 + 1e-13)
+
+
+# --------------------------------------------------------------- round-2 pins
+def test_centroids_left_to_right_order(orc):
+    """O5 (Alg.4 line 6): c_t = (((0 + s_i1) + s_i2) + ...) / |b|
+    with members ascending, bit for bit.  The data mixes magnitudes so that the
+    summation order changes the rounding: a reversed (or pairwise) sum fails."""
+    rng = np.random.default_rng(123)
+    n, d = 3000, 4
+    X = rng.random((n, d)) * 10.0 ** rng.integers(-6, 7, size=(n, d))
+    scale_ = np.array([0.3, 1.7, 0.05, 3.1])
+    S = orc.scale(X, scale_)
+    k = 37
+    bo = rng.integers(0, k, size=n).astype(np.int32)
+    perm, off = orc.layout(bo, k)
+    C = orc.centroids(S, perm, off)
+    differs = 0
+    for t in range(k):
+        members = perm[off[t]:off[t + 1]]
+        assert list(members) == sorted(members)  # O4: ascending original index
+        for j in range(d):
+            acc = 0.0
+            for i in members:  # Python floats are IEEE binary64: one rounding per add
+                acc = acc + float(S[i, j])
+            assert C[t, j] == acc / len(members), (t, j)
+            rev = 0.0
+            for i in members[::-1]:
+                rev = rev + float(S[i, j])
+            differs += (rev / len(members)) != C[t, j]
+    assert differs > 0  # the pin can tell the orders apart on this data
+
+
+def test_block_term_at_equals_loglik_terms(orc):
+    """orc_block_term_at (used by the sampled cfg2/cfg4 parity tests) returns the
+    same term as orc_loglik's per-block output (bitwise: same arithmetic), and
+    that term equals the explicit-inverse Gaussian conditional."""
+    n, d, bs, m = 600, 4, 12, 25
+    X = si.make_X(n, d, seed=141)
+    y = si.make_y(X, seed=142)
+    theta = np.array([1.2, 0.3, 0.5, 0.9, 0.4, 2.5, 1e-3])
+    P = orc.prepare(X, bs, m, theta[1:1 + d], seed=9)
+    ll, terms, quads, logdets = orc.loglik(X, y, P["perm"], P["off"], P["nbr"], P["cnt"], theta,
+                                           return_terms=True)
+    Sig = dense_cov(X, theta)
+    for t in list(range(0, P["k"], 7)) + [P["k"] - 1]:
+        to, qo, lo = orc.block_term_at(X, y, P["perm"], P["off"], P["nbr"], P["cnt"], t, theta)
+        assert (to, qo, lo) == (terms[t], quads[t], logdets[t]), t
+        B = P["perm"][P["off"][t]:P["off"][t + 1]]
+        J = P["nbr"][t, :P["cnt"][t]]
+        if len(J):
+            W = Sig[np.ix_(B, J)] @ np.linalg.inv(Sig[np.ix_(J, J)])
+            mu, C = W @ y[J], Sig[np.ix_(B, B)] - W @ Sig[np.ix_(J, B)]
+        else:
+            mu, C = np.zeros(len(B)), Sig[np.ix_(B, B)]
+        ref = stats.multivariate_normal(mean=mu, cov=C).logpdf(y[B])
+        assert abs(to - ref) <= 1e-9 * max(1.0, abs(ref)), t
