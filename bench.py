@@ -8,8 +8,10 @@ synthetic workload: sbv_prepare_h (scale, RAC, zeta order, layout, centroids,
 kNN) + sbv_loglik (staging, fused per-block Cholesky kernel, reductions, and
 the NCCL exchange when N > 1), inputs resident in HBM.  Workload at N=1:
 BASELINE.json configs[1] (n=1M, d=10, bs=100, m=200, one eval on 1 B200).
-N > 1 (torchrun, one process per GPU) evaluates the SAME problem with blocks
-sharded across ranks (strong scaling).  Rank 0 prints one JSON line.
+N > 1 (one process per GPU: torchrun, or spawned by bench.py itself when
+WORLD_SIZE is unset) evaluates the SAME problem with blocks sharded across ranks
+(strong scaling); --config cfg5 is the weak-scaling workload (5M points per
+GPU).  Rank 0 prints one JSON line.
 
 --impl reference times the CPU oracle (oracle/, the "reference arm" for this
 tier) on the box's host cores on a bounded sample of the same workload and
@@ -101,16 +103,29 @@ class Clocks:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
-def workload(cfg: str):
+def workload(cfg: str, ngpu: int = 1):
+    """The workload of a BASELINE.json config; cfg5 is weak scaling at 5M
+    points per GPU (n = 5M x N)."""
     c = dict(si.CONFIGS[cfg])
+    if cfg == "cfg5":
+        c["n"] = si.CONFIGS["cfg5"]["n"] * ngpu
     return c
 
 
 # ----------------------------------------------------------------------------- reference arm
-def oracle_sample(c, n_s: int, nthreads: int):
-    """Time the oracle (as it stands) on an n_s-point sample of the workload and
-    scale to one full eval with the path's complexity: prepare (RAC n*k + kNN
-    n*k/2 pair work) ~ n^2, loglik ~ number of blocks."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_run(c, n_s: int, nthreads: int):
+    """The oracle (as it stands) on an n_s-point instance of the workload
+    (same d/bs/m/theta): (prepare seconds, loglik seconds, ell)."""
     import oracle
     d, bs, m, nu = c["d"], c["bs"], c["m"], c["nu"]
     X = si.make_X(n_s, d, seed=1)
@@ -122,11 +137,72 @@ def oracle_sample(c, n_s: int, nthreads: int):
     t1 = time.perf_counter()
     ll = oracle.loglik(X, y, P["perm"], P["off"], P["nbr"], P["cnt"], theta, nthreads=nthreads)
     t2 = time.perf_counter()
-    r = c["n"] / n_s
-    t_full = (t1 - t0) * r * r + (t2 - t1) * r
-    return dict(t_prep=t1 - t0, t_llh=t2 - t1, t_full=t_full, ll=ll,
-                sample=f"oracle prepare+loglik on n={n_s} points of the {c['n']}-point workload "
-                       f"(same d/bs/m/theta), scaled to n={c['n']} as prepare*(n/n_s)^2 + loglik*(n/n_s)")
+    return t1 - t0, t2 - t1, ll
+
+
+REF_SAMPLES = (100_000, 200_000, 300_000)  # oracle sample sizes (both arms)
+
+
+def fit_oracle_model(c, nthreads, samples=REF_SAMPLES):
+    """Fit the oracle's cost on several sample sizes of the workload:
+    prepare(n) = a n^2 + b n^2 ln n (RAC n k pairs + the full-sort kNN,
+    sum_t off_t ln off_t ~ n^2/(2bs) ln n), loglik(n) = c n (k = n/bs blocks of
+    a fixed size mix).  Returns the fitted coefficients, the per-sample
+    measurements and the model's worst relative error on them."""
+    rows = []
+    for n_s in samples:
+        tp, tl, _ = oracle_run(c, n_s, nthreads)
+        rows.append((n_s, tp, tl))
+    n = np.array([r[0] for r in rows], dtype=np.float64)
+    tp = np.array([r[1] for r in rows])
+    tl = np.array([r[2] for r in rows])
+    A = np.stack([n * n, n * n * np.log(n)], axis=1)
+    coef, *_ = np.linalg.lstsq(A / tp[:, None], np.ones_like(tp), rcond=None)  # relative LSQ
+    if coef[1] < 0:  # keep the model monotone: fall back to a pure n^2 ln n law
+        coef = np.array([0.0, np.mean(tp / (n * n * np.log(n)))])
+    cl = float(np.mean(tl / n))
+    pred_p = A @ coef
+    err = float(np.max(np.abs(pred_p - tp) / tp))
+    err_l = float(np.max(np.abs(cl * n - tl) / tl))
+    return dict(a=float(coef[0]), b=float(coef[1]), c=cl, rows=rows, err_prepare=err, err_loglik=err_l)
+
+
+def model_seconds(mod, n):
+    return mod["a"] * n * n + mod["b"] * n * n * math.log(n), mod["c"] * n
+
+
+def cpu_baseline_measure(c, name):
+    """SURVEY 8(d) oracle timing on the box's host cores: cfg1 in full, the
+    configured workload by a fitted model over 3 sample sizes, a 1-thread
+    pass, prepare and loglik reported separately."""
+    nth = os.cpu_count() or 1
+    c1 = si.CONFIGS["cfg1"]
+    t1p, t1l, _ = oracle_run(c1, c1["n"], nth)
+    if c["n"] <= REF_SAMPLES[-1]:
+        s1p, s1l, _ = oracle_run(c, c["n"], 1)
+        return {"value": 1.0 / (t1p + t1l) if c is c1 else None, "unit": "evals/s", "cores": nth,
+                "kind": "oracle", "cpu_model": cpu_model(), "sample": "the full workload",
+                "one_thread": {"n": c["n"], "prepare_s": s1p, "loglik_s": s1l},
+                "cfg1_full": {"n": c1["n"], "prepare_s": t1p, "loglik_s": t1l, "evals_s": 1.0 / (t1p + t1l)}}
+    mod = fit_oracle_model(c, nth)
+    n_full = c["n"]
+    tp, tl = model_seconds(mod, n_full)
+    s1p, s1l, _ = oracle_run(c, REF_SAMPLES[0], 1)
+    return {
+        "value": 1.0 / (tp + tl), "unit": "evals/s", "cores": nth, "kind": "oracle",
+        "cpu_model": cpu_model(),
+        "sample": (f"oracle (plain C, OpenMP over blocks) run in full at n = "
+                   f"{', '.join(str(r[0]) for r in mod['rows'])} of the {name} workload (same d/bs/m/theta), "
+                   f"extrapolated to n = {n_full} by prepare = a n^2 + b n^2 ln n, loglik = c n "
+                   f"(least squares; worst fit error {mod['err_prepare']:.1%} / {mod['err_loglik']:.1%})"),
+        "extrapolated_prepare_s": tp, "extrapolated_loglik_s": tl,
+        "samples": [{"n": r[0], "prepare_s": r[1], "loglik_s": r[2]} for r in mod["rows"]],
+        "model": {"a": mod["a"], "b": mod["b"], "c": mod["c"],
+                  "max_rel_err_prepare": mod["err_prepare"], "max_rel_err_loglik": mod["err_loglik"]},
+        "one_thread": {"n": REF_SAMPLES[0], "prepare_s": s1p, "loglik_s": s1l},
+        "cfg1_full": {"n": c1["n"], "prepare_s": t1p, "loglik_s": t1l, "evals_s": 1.0 / (t1p + t1l),
+                      "cores": nth},
+    }
 
 
 def run_reference(args):
@@ -135,29 +211,50 @@ def run_reference(args):
         return 0
     import oracle
     oracle.build()
-    c = workload(args.config)
+    c = workload(args.config, args.gpus)
     nthreads = os.cpu_count() or 1
-    n_s = args.ref_sample or 200_000
+    if c["n"] <= REF_SAMPLES[-1]:  # small workloads (cfg1): the oracle runs in full
+        mod, n_s = None, c["n"]
+        mp = ml = fp = fl = 1.0
+    else:
+        # the cost model's shape from the three sample sizes (once), then every
+        # step is the oracle at the middle sample size scaled by that model
+        mod = fit_oracle_model(c, nthreads)
+        n_s = REF_SAMPLES[1]
+        mp, ml = model_seconds(mod, n_s)
+        fp, fl = model_seconds(mod, c["n"])
     for _ in range(args.warmup):
-        oracle_sample(c, n_s, nthreads)
-    times = []
-    last = None
+        oracle_run(c, n_s, nthreads)
+    times, tps, tls = [], [], []
     for _ in range(args.steps):
-        last = oracle_sample(c, n_s, nthreads)
-        times.append(last["t_full"])
+        tp, tl, _ = oracle_run(c, n_s, nthreads)
+        tps.append(tp)
+        tls.append(tl)
+        times.append(tp * fp / mp + tl * fl / ml)
     t = statistics.mean(times)
     val = 1.0 / t
     out = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "evals/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": scaling_kind(args.config), "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config_dict(c, args.config, args.gpus),
         "cpu_baseline": {"value": val, "unit": "evals/s", "cores": nthreads, "kind": "oracle",
-                         "sample": last["sample"]},
+                         "cpu_model": cpu_model(),
+                         "sample": (f"each step: the oracle in full (prepare {statistics.mean(tps):.2f} s + "
+                                    f"loglik {statistics.mean(tls):.2f} s)" if mod is None else
+                                    f"each step: the oracle at n = {n_s} of the workload (prepare "
+                                    f"{statistics.mean(tps):.2f} s + loglik {statistics.mean(tls):.2f} s), scaled "
+                                    f"to n = {c['n']} by the model fitted at n = {REF_SAMPLES} "
+                                    f"(prepare = a n^2 + b n^2 ln n, loglik = c n; worst fit error "
+                                    f"{mod['err_prepare']:.1%})")},
         "e2e": {"value": val, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out))
     return 0
+
+
+def scaling_kind(name):
+    return "weak" if name == "cfg5" else "strong"
 
 
 def config_dict(c, name, ngpu):
@@ -180,9 +277,8 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+    if world != args.gpus and world == 1 and args.gpus > 1:
+        raise SystemExit("internal: N > 1 without torchrun")
     os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -193,7 +289,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     peaks, fp64_peak = load_peaks()
-    c = workload(args.config)
+    c = workload(args.config, world)
     n, d, bs, m, nu = c["n"], c["d"], c["bs"], c["m"], c["nu"]
     X_h = si.make_X(n, d, seed=1)
     y_h = si.make_y(X_h, seed=2, kind="iid")
@@ -241,8 +337,11 @@ def run_ours(args):
             stage_llh.setdefault(k_, []).append(v)
     torch.cuda.synchronize()
     ck = clocks.stop()
+    ck_all = [ck]
     if world > 1:
         dist.barrier()
+        ck_all = [None] * world
+        dist.all_gather_object(ck_all, ck)
     ms = sum(a.elapsed_time(b) for a, b in zip(e0, e1)) / args.steps
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -350,19 +449,23 @@ def run_ours(args):
         stages_max = {k_: max(s.get(k_, 0.0) for s in stages_all) for k_ in stages}
         stages_min = {k_: min(s.get(k_, 0.0) for s in stages_all) for k_ in stages}
         dom = max(((k_, v) for k_, v in stages.items() if "H" in k_), key=lambda kv: kv[1])
-        h8_tf = flops_total / (h8_ms_max * 1e-3) / 1e12
+        h8_tf = flops_total / (h8_ms_max * 1e-3) / 1e12        # all GPUs
+        h8_tf_gpu = flops_total / world / (h8_ms_max * 1e-3) / 1e12  # per GPU (slowest rank's time)
         roof = roofline(dom, stats, c, fp64_peak, peaks, world, h8_ms_max, flops_total, h8_bytes_total)
+        reasons = sorted({r for ckr in ck_all for r in (ckr.get("reasons") or [])})
+        sm_all = [ckr.get("sm_mhz") for ckr in ck_all if ckr.get("sm_mhz") is not None]
         out = {
             "metric": METRIC, "value": evals_s, "unit": "evals/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": config_dict(c, args.config, world),
+            "higher_is_better": True, "scaling": scaling_kind(args.config), "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": config_dict(c, args.config, world),
             "tflops_step": flops_total / (ms_max * 1e-3) / 1e12,
             "loglik_only": {"evals_s": 1e3 / llh_ms_max, "ms": llh_ms_max,
                             "tflops": flops_total / (llh_ms_max * 1e-3) / 1e12,
-                            "h8_ms": h8_ms_max, "h8_tflops": h8_tf,
-                            "h8_frac_of_fp64_peak": h8_tf / fp64_peak,
-                            "fp64_peak_tflops": fp64_peak, "flops_per_eval": flops_total},
+                            "h8_ms": h8_ms_max, "h8_tflops_all_gpus": h8_tf,
+                            "h8_tflops_per_gpu": h8_tf_gpu,
+                            "h8_frac_of_fp64_peak_per_gpu": h8_tf_gpu / fp64_peak,
+                            "fp64_peak_tflops_per_gpu": fp64_peak, "flops_per_eval": flops_total},
             "stage_ms_rank0": stages,
             **({"stage_ms_max_over_ranks": stages_max, "stage_ms_min_over_ranks": stages_min}
                if world > 1 else {}),
@@ -372,18 +475,15 @@ def run_ours(args):
                     "h2d_bytes_per_step": int(n * d * 8 + n * 8), "d2h_bytes_per_step": 8 * 8},
             "gpu_launches": launches,
             **({"predict": pred} if pred else {}),
-            "clocks": ck,
+            "clocks": {**ck, "reasons": reasons,
+                       **({"sm_mhz_min_over_ranks": min(sm_all), "per_rank": ck_all} if world > 1 else {})},
             "ll": ll,
             "realised": stats,
         }
         if world == 1 and not args.no_cpu_baseline:
             import oracle
             oracle.build()
-            nth = os.cpu_count() or 1
-            r = oracle_sample(c, args.ref_sample or 400_000, nth)
-            out["cpu_baseline"] = {"value": 1.0 / r["t_full"], "unit": "evals/s", "cores": nth,
-                                   "kind": "oracle", "sample": r["sample"],
-                                   "sample_seconds": r["t_prep"] + r["t_llh"]}
+            out["cpu_baseline"] = cpu_baseline_measure(c, args.config)
         print(json.dumps(out))
     if world > 1:
         dist.barrier()
@@ -439,21 +539,35 @@ def roofline(dom, stats, c, fp64_peak, peaks, world, h8_ms, flops_total, h8_byte
             "frac": None, "traffic": None}
 
 
+def spawn_ranks(args):
+    """--gpus N > 1 without torchrun: launch N local ranks (one process per
+    GPU) with torch.distributed.run on 127.0.0.1 and pass rank 0's line through."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    r = subprocess.run(cmd, cwd=ROOT)
+    return r.returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2")
-    ap.add_argument("--ref-sample", type=int, default=None,
-                    help="oracle sample size (default: 400k for the cpu_baseline leg, 200k per "
-                         "--impl reference step so K + W steps stay within a few minutes)")
+    ap.add_argument("--config", default="cfg2",
+                    help="cfg1..cfg5 (BASELINE.json configs); cfg5 = weak scaling, 5M points per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-predict", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

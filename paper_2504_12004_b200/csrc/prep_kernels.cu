@@ -292,13 +292,17 @@ __global__ void k_iota(int64_t n, int32_t *v) {
     v[i] = (int32_t)i;
 }
 
+// off[b] = first sorted position with block id >= b, for every b in [0, k]
+// (empty blocks, possible with a caller-given partition, get off[b] = off[b+1])
 __global__ void k_offsets(const int32_t *sorted_block, int64_t n, int64_t k, int64_t *off) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x) {
-    int32_t b = sorted_block[p];
-    if (p == 0 || sorted_block[p - 1] != b) off[b] = p;  // every block is non-empty
+    const int32_t b = sorted_block[p];
+    const int32_t prev = p == 0 ? -1 : sorted_block[p - 1];
+    for (int32_t c = prev + 1; c <= b; c++) off[c] = p;
+    if (p == n - 1)
+      for (int64_t c = (int64_t)b + 1; c <= k; c++) off[c] = n;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) off[k] = n;
 }
 
 // Block-major layout: a stable radix sort of (block id -> original index)

@@ -5,7 +5,11 @@
 // llh_kernel.cu).  No host arithmetic of the method happens here: the host
 // only validates arguments, sizes buffers, builds the block shard / work
 // order from the device-computed layout, and launches.
+#include <dlfcn.h>
+#include <execinfo.h>
 #include <math.h>
+#include <signal.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -258,6 +262,10 @@ struct Timer {
     if (h->profile) cudaEventRecord(h->ev[0], h->stream);
   }
   void mark(const char *name) {
+    if (h->debug) {  // SBV_DEBUG=1: stage trace on stderr (host-side progress)
+      fprintf(stderr, "[sbv] %s %s done (queued)\n", prep ? "prepare" : "loglik", name);
+      fflush(stderr);
+    }
     if (!h->profile || idx >= kMaxStages) return;
     cudaEventRecord(h->ev[idx + 1], h->stream);
     (prep ? h->name_prep : h->name_llh)[idx] = name;
@@ -364,6 +372,24 @@ int sbv_shard_blocks(int64_t bc, int32_t rank, int32_t world, int32_t *blocks, i
   return SBV_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// SBV_DEBUG=1: print the native stack on SIGSEGV (host-side debugging aid)
+void segv_handler(int sig) {
+  void *frames[64];
+  const int nf = backtrace(frames, 64);
+  fprintf(stderr, "[sbv] signal %d, native backtrace:\n", sig);
+  backtrace_symbols_fd(frames, nf, 2);
+  Dl_info info;
+  if (dladdr((void *)&segv_handler, &info)) fprintf(stderr, "[sbv] libsbv base %p\n", info.dli_fbase);
+  signal(sig, SIG_DFL);
+  raise(sig);
+}
+}  // namespace
+
+extern "C" {
+
 int sbv_create(const sbv_opts *opts, sbv_handle *out) {
   if (!out) return SBV_ERR_ARG;
   *out = nullptr;
@@ -377,6 +403,9 @@ int sbv_create(const sbv_opts *opts, sbv_handle *out) {
   {
     const char *e = getenv("SBV_GRID");
     h->use_grid = (e && atoi(e) == 0) ? 0 : 1;
+    const char *dbg = getenv("SBV_DEBUG");
+    h->debug = (dbg && atoi(dbg) != 0) ? 1 : 0;
+    if (h->debug) signal(SIGSEGV, segv_handler);
   }
   if (opts) {
     h->seed = opts->seed;
@@ -599,6 +628,12 @@ int prepare_impl(sbv_ctx *h, const double *X, int64_t n, int32_t d, int32_t bs, 
   CU(cudaEventRecord(h->ev_sizes, st));
   if (given_bo) {  // a caller partition is validated before H5-H6 run on it
     CU(cudaEventSynchronize(h->ev_sizes));
+    if (h->debug) {
+      fprintf(stderr, "[sbv] given partition: k=%lld off[0..3]=%lld %lld %lld %lld off[k]=%lld flag=%d\n",
+              (long long)k, (long long)off_h[0], (long long)off_h[std::min<int64_t>(1, k)],
+              (long long)off_h[std::min<int64_t>(2, k)], (long long)off_h[std::min<int64_t>(3, k)],
+              (long long)off_h[k], *h->flag_host);
+    }
     if (*h->flag_host) return fail(h, SBV_ERR_ARG, "X/scale non-finite or block id out of [0, k)");
     for (int64_t t = 0; t < k; t++)
       if (off_h[t + 1] == off_h[t]) return fail(h, SBV_ERR_ARG, "given partition has an empty block");
@@ -632,6 +667,11 @@ int prepare_impl(sbv_ctx *h, const double *X, int64_t n, int32_t d, int32_t bs, 
   if (*h->flag_host)
     return fail(h, SBV_ERR_ARG, given_bo ? "X/scale non-finite or block id out of [0, k)"
                                          : "X has non-finite entries (or X/scale overflows)");
+  // the layout as the host sees it must be a partition of [0, n) (guards the
+  // host-side sizing below against a failed device step)
+  if (off_h[0] != 0 || off_h[k] != n) return fail(h, SBV_ERR_CUDA, "block layout inconsistent (device step failed)");
+  for (int64_t t = 0; t < k; t++)
+    if (off_h[t + 1] < off_h[t]) return fail(h, SBV_ERR_CUDA, "block layout inconsistent (device step failed)");
   for (int64_t li = 0; li < h->k_local; li++) cnt_h[li] = (int32_t)std::min<int64_t>(m, off_h[local[li]]);
   std::vector<int32_t> Nt(h->k_local);
   h->max_N = 0;

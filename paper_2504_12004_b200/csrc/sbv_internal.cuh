@@ -45,6 +45,7 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   uint64_t seed = 3;
   int profile = 0;
+  int debug = 0;  // SBV_DEBUG=1: host-side stage trace on stderr
   // comm
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;

@@ -29,11 +29,14 @@ __global__ void k_lat(int kind, int iters, double seed, long long *out, double *
     for (int i = 0; i < iters; i++) a = exp_neg(a) + 0.5;
   } else if (kind == 6) {
     for (int i = 0; i < iters; i++) a = sqrt(a) + 1.0;
+  } else if (kind == 7) {
+    for (int i = 0; i < iters; i++) a = rsqrt_pos(a) + 1.0;
   }
   long long t1 = clock64();
   if (threadIdx.x == 0) out[0] = t1 - t0;
   sink[threadIdx.x] = a + c0 + c1;
 }
+
 
 // both factorisations of one tile: outputs of diag_factor (old) and
 // diag_factor2 (new) written to out[0..2*32*kDld*2)
@@ -121,8 +124,8 @@ int main() {
   double *sink;
   cudaMalloc(&d_out, 16 * sizeof(long long));
   cudaMalloc(&sink, 4096 * sizeof(double));
-  const char *names[] = {"dfma", "dmma_acc", "shfl_f64", "rsqrt_f64", "log_f64", "exp_neg", "sqrt_f64"};
-  for (int kind = 0; kind < 7; kind++) {
+  const char *names[] = {"dfma", "dmma_acc", "shfl_f64", "rsqrt_f64", "log_f64", "exp_neg", "sqrt_f64", "rsqrt_pos"};
+  for (int kind = 0; kind < 8; kind++) {
     const int iters = 4096;
     k_lat<<<1, 32>>>(kind, iters, 1.5, d_out, sink);
     long long cyc;
