@@ -43,7 +43,7 @@ def analyse(path):
     typ = (code >> 24) & 0xFF
     j = (code >> 12) & 0xFFF
     ch = code & 0xFFF
-    names = {0: "A", 1: "F", 2: "C0", 3: "BC"}
+    names = {0: "A", 1: "F", 2: "C0", 3: "BC", 4: "BCF"}
     res = {"records": int(len(r))}
     task = typ < 0xF0
     # per-CTA span: first record to last record
@@ -81,9 +81,10 @@ def analyse(path):
     res["block_span_cycles_mean"] = float(np.mean(bspan)) if bspan else None
     res["block_N_mean"] = float(np.mean(nlist)) if nlist else None
     # F-chain: end of F(j) -> end of F(j+1) within a block
-    fm = task & (typ == 1)
-    order = np.lexsort((j[fm], item[fm]))
-    fi, fj, fe, fs, fr = item[fm][order], j[fm][order], t2[fm][order], t0[fm][order], t1[fm][order]
+    fm = task & ((typ == 1) | (typ == 4))  # F(j) or BCF(j-1) = BC(j-1,1) + F(j)
+    jf = np.where(typ == 4, j + 1, j)
+    order = np.lexsort((jf[fm], item[fm]))
+    fi, fj, fe, fs, fr = item[fm][order], jf[fm][order], t2[fm][order], t0[fm][order], t1[fm][order]
     gaps = []
     for a_ in range(1, len(fi)):
         if fi[a_] == fi[a_ - 1] and fj[a_] == fj[a_ - 1] + 1:
