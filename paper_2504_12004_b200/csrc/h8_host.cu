@@ -101,6 +101,7 @@ cudaError_t launch_h8_problem(const H8Problem &pb, int d, const double *theta, u
   a.status = pb.status;
   a.np_max = h8_np_max(pb.max_N);
   a.max_tasks = h8_max_tasks(pb.max_N);
+  a.max_N = pb.max_N;
   a.predict = pb.predict;
   a.Xq = pb.Xq;
   a.pmean = pb.pmean;
@@ -109,8 +110,6 @@ cudaError_t launch_h8_problem(const H8Problem &pb, int d, const double *theta, u
   cudaError_t e = cudaMemsetAsync(queue, 0, sizeof(unsigned int), st);
   if (e) return e;
   if (pb.k_local == 0) return cudaSuccess;
-  const H8Fn f = pick(nu, d, pb.predict);
-  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pb.smem);
   a.trace = nullptr;
   a.trace_n = nullptr;
   a.trace_cap = 0;
@@ -127,7 +126,11 @@ cudaError_t launch_h8_problem(const H8Problem &pb, int d, const double *theta, u
   a.trace_n = tn;
   a.trace_cap = cap;
 #endif
-  f<<<pb.grid, kH8Threads, pb.smem, st>>>(a);
+  {
+    const H8Fn f = pick(nu, d, pb.predict);
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pb.smem);
+    f<<<pb.grid, kH8Threads, pb.smem, st>>>(a);
+  }
 #if SBV_TRACE
   if (const char *out = getenv("SBV_TRACE_OUT")) {
     unsigned int n = 0;
