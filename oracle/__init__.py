@@ -81,6 +81,11 @@ def lib():
         L.orc_predict_block.argtypes = [_p, _p, _p, _i32, _p, _i32, _p, _i32, _p, _p, _p]
         L.orc_predict_block.restype = ctypes.c_int
         L.orc_simulate.argtypes = [_p, _p, _i64, _i32, _u64, _dbl, _p, _p, _p, _p]
+        L.orc_kernel_grad.argtypes = [_p, _p, _i32, _p, _i32, _p]
+        L.orc_block_grad.argtypes = [_p, _p, _i32, _p, _i32, _p, _i32, _p, _p]
+        L.orc_block_grad.restype = ctypes.c_int
+        L.orc_loglik_grad.argtypes = [_p, _p, _i32, _p, _p, _i64, _p, _p, _i32, _p, _i32, _p, _p]
+        L.orc_loglik_grad.restype = ctypes.c_int
         L.orc_z_crit.argtypes = [_dbl]
         L.orc_z_crit.restype = _dbl
         _lib = L
@@ -338,6 +343,56 @@ def predict(Xtr, y, Xte, bs_pred: int, m_pred: int, scale_, theta, seed: int = 3
         var[B] = v
         nbrs.append(J)
     return mean, var, dict(anchors=anc, block_of=bo, perm=perm, off=off, C=C, nbr=nbrs)
+
+
+# ----------------------------------------------------------------- O13 (NEXT N3)
+def kernel_grad(xa, xb, theta, same: bool):
+    """d K(xa, xb) / d (sigma2, beta_1..beta_d, tau2)."""
+    xa, pa = _c(xa, np.float64)
+    xb, pb = _c(xb, np.float64)
+    th, pt = _c(theta, np.float64)
+    out = np.empty(xa.shape[0] + 2)
+    lib().orc_kernel_grad(pa, pb, xa.shape[0], pt, int(same), out.ctypes.data_as(_p))
+    return out
+
+
+def block_grad(X, y, J, B, theta):
+    """d ell_t / d (sigma2, beta, tau2) of one block (Alg.5 term, nu fixed)."""
+    X, px = _c(X, np.float64)
+    y, py = _c(y, np.float64)
+    J, pj = _c(np.asarray(J, dtype=np.int32).reshape(-1), np.int32)
+    B, pB = _c(np.asarray(B, dtype=np.int32).reshape(-1), np.int32)
+    th, pt = _c(theta, np.float64)
+    g = np.empty(X.shape[1] + 2)
+    rc = lib().orc_block_grad(px, py, X.shape[1], pj, J.shape[0], pB, B.shape[0], pt, g.ctypes.data_as(_p))
+    if rc == 4:
+        raise NotPD(-1, 0)
+    if rc != 0:
+        raise ValueError("gradient needs a half-integer nu")
+    return g
+
+
+def loglik_grad(X, y, perm, off, nbr, cnt, theta, nthreads: int = 0, return_blocks=False):
+    """sum over blocks of d ell_t / d (sigma2, beta, tau2)."""
+    X, px = _c(X, np.float64)
+    y, py = _c(y, np.float64)
+    perm, pp = _c(perm, np.int32)
+    off, po = _c(off, np.int64)
+    k = off.shape[0] - 1
+    m = nbr.shape[1] if nbr.ndim == 2 else 0
+    nbr_, pn = _c(nbr if m > 0 else np.zeros((k, 1), np.int32), np.int32)
+    cnt, pc = _c(cnt, np.int32)
+    th, pt = _c(theta, np.float64)
+    P = X.shape[1] + 2
+    g = np.empty(P)
+    gb = np.empty((k, P))
+    rc = lib().orc_loglik_grad(px, py, X.shape[1], pp, po, k, pn, pc, max(m, 1), pt, nthreads,
+                               g.ctypes.data_as(_p), gb.ctypes.data_as(_p))
+    if rc == 4:
+        raise NotPD(-1, 0)
+    if rc != 0:
+        raise ValueError("gradient needs a half-integer nu")
+    return (g, gb) if return_blocks else g
 
 
 def z_crit(ci_level: float) -> float:

@@ -32,6 +32,9 @@
  *   O11 orc_predict_block  Sec.4.1 restricted to NN(B*_j):
  *                       mu = Sigma_{*J} Sigma_JJ^-1 y_J, var = diag(Sigma_** - Sigma_{*J}
  *                       Sigma_JJ^-1 Sigma_{J*}); Sec.5.5
+ *   O13 orc_block_grad  NEXT row N3 ("gradient quantities"): d ell_t / d theta
+ *                       (sigma2, beta, tau2) from Eq.1 differentiated, joint minus
+ *                       marginal; orc_loglik_grad sums the blocks
  *   O12 orc_simulate    Sec.5.5: n_sim draws N(mu_j, var_j) per point,
  *                       sample mean / sd / (1 - alpha) interval
  *
@@ -475,6 +478,181 @@ int orc_loglik(const double *X, const double *y, int64_t n, int32_t d,
 }
 
 /* Single-block variant used by sampled parity checks at full size. */
+/* ------------------------------------------------------------------ O13 */
+/* NEXT row N3, the gradient quantities of P:453: d ell_t /
+ * d theta for theta = (sigma2, beta_1..beta_d, tau2), nu held fixed (the
+ * half-integer closed forms are a discrete family; Q28).
+ *
+ * Alg.5's term is the Gaussian conditional of y_B given y_J, i.e. the joint
+ * density of [y_J; y_B] minus the marginal of y_J, so Eq.1
+ * differentiated twice gives, with K = K([J; B]), K_JJ = K(J, J),
+ * K_k = dK/d theta_k, alpha = K^-1 [y_J; y_B], alpha_J = K_JJ^-1 y_J:
+ *   d ell_t / d theta_k = 1/2 (alpha^T K_k alpha - tr(K^-1 K_k))
+ *                       - 1/2 (alpha_J^T K_k,JJ alpha_J - tr(K_JJ^-1 K_k,JJ)).
+ * Entries of K_k (Eq.5-6 differentiated, paper parameterisation):
+ *   d/d sigma2 = f(r) (Matern with sigma2 = 1; no nugget),
+ *   d/d beta_j = sigma2 f'(r) dr/d beta_j, dr/d beta_j = -(dx_j / beta_j)^2 / (beta_j r)
+ *                (0 at r = 0),
+ *   d/d tau2   = 1 on the same-point diagonal (Q3),
+ * f'(r): nu=1/2: -e^-r; 3/2: -r e^-r; 5/2: -(r/3)(1+r) e^-r; 7/2: -(r/15)(3+3r+r^2) e^-r.
+ * Explicit inverses by Cholesky (chol_lower) and forward/back substitution of
+ * the identity; plain loops.  Returns ORC_ERR_NOT_PD if K or K_JJ is not PD,
+ * ORC_ERR_ARG for a nu without a closed form. */
+static double matern_unit(double r, double nu, double *dfdr) {
+  const double e = exp(-r);
+  if (nu == 0.5) {
+    *dfdr = -e;
+    return e;
+  }
+  if (nu == 1.5) {
+    *dfdr = -r * e;
+    return (1.0 + r) * e;
+  }
+  if (nu == 2.5) {
+    *dfdr = -(r / 3.0) * (1.0 + r) * e;
+    return (1.0 + r + r * r / 3.0) * e;
+  }
+  if (nu == 3.5) {
+    *dfdr = -(r / 15.0) * (3.0 + 3.0 * r + r * r) * e;
+    return (1.0 + r + 2.0 * r * r / 5.0 + r * r * r / 15.0) * e;
+  }
+  *dfdr = NAN;
+  return NAN;
+}
+
+void orc_kernel_grad(const double *xa, const double *xb, int32_t d, const double *theta,
+                     int32_t same_point, double *out) {
+  const double *beta = theta + 1;
+  const double r = orc_scaled_distance(xa, xb, d, beta);
+  double fp;
+  const double f = matern_unit(r, theta[d + 1], &fp);
+  out[0] = f;
+  for (int32_t j = 0; j < d; j++) {
+    double drdb = 0.0;
+    if (r > 0.0) {
+      const double u = (xa[j] - xb[j]) / beta[j];
+      drdb = -(u * u) / (beta[j] * r);
+    }
+    out[1 + j] = theta[0] * fp * drdb;
+  }
+  out[d + 1] = same_point ? 1.0 : 0.0;
+}
+
+/* explicit inverse of the SPD n x n matrix A (destroyed): Ainv = L^-T L^-1 */
+static int spd_inverse(double *A, int64_t n, double *Ainv) {
+  if (chol_lower(A, n) != 0) return ORC_ERR_NOT_PD;
+  double *col = (double *)malloc(sizeof(double) * (n > 0 ? n : 1));
+  for (int64_t c = 0; c < n; c++) {
+    for (int64_t i = 0; i < n; i++) col[i] = i == c ? 1.0 : 0.0;
+    forward_subst(A, n, col);                 /* L^-1 e_c */
+    for (int64_t i = n - 1; i >= 0; i--) {    /* L^-T (L^-1 e_c) */
+      double s = col[i];
+      for (int64_t q = i + 1; q < n; q++) s = s - A[q * n + i] * col[q];
+      col[i] = s / A[i * n + i];
+    }
+    for (int64_t i = 0; i < n; i++) Ainv[i * n + c] = col[i];
+  }
+  free(col);
+  return ORC_OK;
+}
+
+int orc_block_grad(const double *X, const double *y, int32_t d, const int32_t *J, int32_t mt,
+                   const int32_t *B, int32_t bst, const double *theta, double *grad) {
+  const int64_t m = mt, b = bst, N = m + b, P = d + 2;
+  const double nu = theta[d + 1];
+  if (!(nu == 0.5 || nu == 1.5 || nu == 2.5 || nu == 3.5)) return ORC_ERR_ARG;
+  int32_t *idx = (int32_t *)malloc(sizeof(int32_t) * N);
+  for (int64_t i = 0; i < m; i++) idx[i] = J[i];
+  for (int64_t i = 0; i < b; i++) idx[m + i] = B[i];
+  double *K = (double *)malloc(sizeof(double) * N * N);
+  double *Kinv = (double *)malloc(sizeof(double) * N * N);
+  double *Kk = (double *)malloc(sizeof(double) * P * N * N); /* Kk[k][i][j] */
+  double *KJ = (double *)malloc(sizeof(double) * (m > 0 ? m * m : 1));
+  double *KJinv = (double *)malloc(sizeof(double) * (m > 0 ? m * m : 1));
+  double *alpha = (double *)malloc(sizeof(double) * N);
+  double *alphaJ = (double *)malloc(sizeof(double) * (m > 0 ? m : 1));
+  double *tmp = (double *)malloc(sizeof(double) * P);
+  int rc = ORC_OK;
+  for (int64_t i = 0; i < N; i++)
+    for (int64_t j = 0; j < N; j++) {
+      const double *xa = X + (int64_t)idx[i] * d, *xb = X + (int64_t)idx[j] * d;
+      K[i * N + j] = orc_kernel(xa, xb, d, theta, i == j);
+      orc_kernel_grad(xa, xb, d, theta, i == j, tmp);
+      for (int64_t k = 0; k < P; k++) Kk[(k * N + i) * N + j] = tmp[k];
+    }
+  for (int64_t i = 0; i < m; i++)
+    for (int64_t j = 0; j < m; j++) KJ[i * m + j] = K[i * N + j];
+  if (spd_inverse(K, N, Kinv) != ORC_OK || (m > 0 && spd_inverse(KJ, m, KJinv) != ORC_OK)) {
+    rc = ORC_ERR_NOT_PD;
+    goto done;
+  }
+  for (int64_t i = 0; i < N; i++) {
+    double s = 0.0;
+    for (int64_t j = 0; j < N; j++) s = s + Kinv[i * N + j] * y[idx[j]];
+    alpha[i] = s;
+  }
+  for (int64_t i = 0; i < m; i++) {
+    double s = 0.0;
+    for (int64_t j = 0; j < m; j++) s = s + KJinv[i * m + j] * y[idx[j]];
+    alphaJ[i] = s;
+  }
+  for (int64_t k = 0; k < P; k++) {
+    const double *D = Kk + k * N * N;
+    double t1 = 0.0, t2 = 0.0, t3 = 0.0, t4 = 0.0;
+    for (int64_t i = 0; i < N; i++)
+      for (int64_t j = 0; j < N; j++) {
+        t1 = t1 + alpha[i] * D[i * N + j] * alpha[j];
+        t2 = t2 + Kinv[i * N + j] * D[j * N + i];
+      }
+    for (int64_t i = 0; i < m; i++)
+      for (int64_t j = 0; j < m; j++) {
+        t3 = t3 + alphaJ[i] * D[i * N + j] * alphaJ[j];
+        t4 = t4 + KJinv[i * m + j] * D[j * N + i];
+      }
+    grad[k] = 0.5 * (t1 - t2) - 0.5 * (t3 - t4);
+  }
+done:
+  free(idx);
+  free(K);
+  free(Kinv);
+  free(Kk);
+  free(KJ);
+  free(KJinv);
+  free(alpha);
+  free(alphaJ);
+  free(tmp);
+  return rc;
+}
+
+/* sum of the block gradients over all blocks (zeta order, plain sums);
+ * grads: optional per-block output [k][d+2] */
+int orc_loglik_grad(const double *X, const double *y, int32_t d, const int32_t *perm,
+                    const int64_t *off, int64_t k, const int32_t *nbr, const int32_t *cnt,
+                    int32_t m, const double *theta, int32_t nthreads, double *grad,
+                    double *grads) {
+  const int64_t P = d + 2;
+  double *g = (double *)malloc(sizeof(double) * k * P);
+  int32_t *st = (int32_t *)calloc(k, sizeof(int32_t));
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic)
+  for (int64_t t = 0; t < k; t++)
+    st[t] = orc_block_grad(X, y, d, nbr + t * (int64_t)m, cnt[t], perm + off[t],
+                           (int32_t)(off[t + 1] - off[t]), theta, g + t * P);
+  int rc = ORC_OK;
+  for (int64_t p = 0; p < P; p++) grad[p] = 0.0;
+  for (int64_t t = 0; t < k; t++) {
+    if (st[t] != ORC_OK && rc == ORC_OK) rc = st[t];
+    for (int64_t p = 0; p < P; p++) grad[p] = grad[p] + g[t * P + p];
+  }
+  if (grads)
+    for (int64_t i = 0; i < k * P; i++) grads[i] = g[i];
+  free(g);
+  free(st);
+  return rc;
+}
+
 int orc_block_term_at(const double *X, const double *y, int32_t d,
                       const int32_t *perm, const int64_t *off,
                       const int32_t *nbr, const int32_t *cnt, int32_t m,
