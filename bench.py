@@ -424,6 +424,26 @@ def run_ours(args):
                 "simulate_1000_draws_ms_wall": sim_ms,
                 "note": "includes test clustering, prediction-mode kNN over the 1M training points and the fused conditional kernel"}
 
+    # --- NEXT row N3 (gradient), outside the timed step: ell and d ell / d (sigma2, beta, tau2)
+    grad = None
+    if world == 1 and not args.no_predict:
+        try:
+            h.loglik_grad(y, theta)
+            torch.cuda.synchronize()
+            gm = []
+            for _ in range(3):
+                flush.zero_()
+                a.record(stream)
+                h.loglik_grad(y, theta)
+                b.record(stream)
+                torch.cuda.synchronize()
+                gm.append(a.elapsed_time(b))
+            grad = {"ms": statistics.mean(gm), "evals_s": 1e3 / statistics.mean(gm),
+                    "params": d + 2, "vs_loglik_only": statistics.mean(gm) / llh_ms_max,
+                    "note": "sbv_loglik_grad: H8 keeping each block's factor + the gradient kernel (grad_kernel.cu)"}
+        except Exception as ex:  # noqa: BLE001
+            grad = {"error": str(ex)[:200]}
+
     # --- kernel launches in one step (CUPTI via torch.profiler, outside the timed region)
     launches = None
     try:
@@ -475,6 +495,7 @@ def run_ours(args):
                     "h2d_bytes_per_step": int(n * d * 8 + n * 8), "d2h_bytes_per_step": 8 * 8},
             "gpu_launches": launches,
             **({"predict": pred} if pred else {}),
+            **({"gradient": grad} if grad else {}),
             "clocks": {**ck, "reasons": reasons,
                        **({"sm_mhz_min_over_ranks": min(sm_all), "per_rank": ck_all} if world > 1 else {})},
             "ll": ll,

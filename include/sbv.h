@@ -142,6 +142,17 @@ int sbv_prepare_blocks(sbv_handle h, const double *X, int64_t n, int32_t d, int6
  * SBV_ERR_STATE (no prepare), SBV_ERR_CUDA, SBV_ERR_COMM. */
 int sbv_loglik(sbv_handle h, const double *y, const double *theta, double *ll);
 
+/* SURVEY 8(f) NEXT row N3, the "gradient quantities" of P:453: ell and its
+ * gradient with respect to (sigma2, beta_1..beta_d, tau2), nu held fixed
+ * (Q28).  grad: host or device double[d+2] in that order.  Per
+ * block, with L = chol(K([J_t; B_t])) and y' = L^-1 [y_J; y_B]:
+ *   d ell_t / d theta_k = 1/2 sum_ij (at dl^T + dl at^T + dl dl^T - Z Z^T)_ij (dK_k)_ij,
+ *   Z = L^-T E_B, dl = Z y'_B, at = [L11^-T y'_J; 0]
+ * (Eq.1 P:156-158 differentiated for the joint minus the marginal of y_J).
+ * One GPU only (world = 1).  Errors: as sbv_loglik, plus SBV_ERR_UNSUPPORTED
+ * for nu outside {0.5, 1.5, 2.5, 3.5} or world > 1. */
+int sbv_loglik_grad(sbv_handle h, const double *y, const double *theta, double *ll, double *grad);
+
 /* As sbv_loglik, plus parts[0..3] = {ell, sum quad, sum logdet, #points}
  * (host double[4], may be NULL). */
 int sbv_loglik_parts(sbv_handle h, const double *y, const double *theta, double *parts);

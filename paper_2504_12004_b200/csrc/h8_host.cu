@@ -103,6 +103,8 @@ cudaError_t launch_h8_problem(const H8Problem &pb, int d, const double *theta, u
   a.max_tasks = h8_max_tasks(pb.max_N);
   a.max_N = pb.max_N;
   a.predict = pb.predict;
+  a.Lg = pb.Lg;
+  a.lg_off = pb.lg_off;
   a.Xq = pb.Xq;
   a.pmean = pb.pmean;
   a.pvar = pb.pvar;

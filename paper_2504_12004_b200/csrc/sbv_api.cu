@@ -131,6 +131,11 @@ void free_state(sbv_ctx *h) {
   release(h->q_terms);
   release(h->q_quads);
   release(h->q_logdets);
+  release(h->Lg);
+  release(h->lg_off);
+  release(h->zws);
+  release(h->grads);
+  release(h->gsum);
   h->cap.clear();
   h->prepared = false;
 }
@@ -673,7 +678,8 @@ int prepare_impl(sbv_ctx *h, const double *X, int64_t n, int32_t d, int32_t bs, 
   for (int64_t t = 0; t < k; t++)
     if (off_h[t + 1] < off_h[t]) return fail(h, SBV_ERR_CUDA, "block layout inconsistent (device step failed)");
   for (int64_t li = 0; li < h->k_local; li++) cnt_h[li] = (int32_t)std::min<int64_t>(m, off_h[local[li]]);
-  std::vector<int32_t> Nt(h->k_local);
+  std::vector<int32_t> &Nt = h->Nt;
+  Nt.assign(h->k_local, 0);
   h->max_N = 0;
   h->min_bs = INT32_MAX;
   h->max_bs = 0;
@@ -705,6 +711,7 @@ int prepare_impl(sbv_ctx *h, const double *X, int64_t n, int32_t d, int32_t bs, 
   CU(ensure(h->work_order, h->k_local, unused));
   CU(cudaMemcpyAsync(h->work_order, order, h->k_local * sizeof(int32_t),
                      cudaMemcpyHostToDevice, st));
+  h->order_h.assign(order, order + h->k_local);
   CU(cudaEventRecord(h->ev_pin, st));  // the next prepare waits on it before reusing `pin`
 
   // per-eval buffers
@@ -855,6 +862,150 @@ int sbv_loglik(sbv_handle h, const double *y, const double *theta, double *ll) {
   int rc = run_loglik(h, y, theta);
   *ll = rc == SBV_OK ? h->result_host[0] : NAN;
   return rc;
+}
+
+// ell and d ell / d (sigma2, beta, tau2).  H8 runs in its
+// factor-keeping mode over batches of blocks (LPT order) that fit the
+// per-block factor copies in SBV_GRAD_BATCH_GB (default 16 GB), each batch
+// followed by the gradient kernel; then the usual H9 reduction for ell and a
+// fixed-order sum of the per-block gradients.
+int sbv_loglik_grad(sbv_handle h, const double *y, const double *theta, double *ll, double *grad) {
+  if (!h) return SBV_ERR_ARG;
+  if (!ll || !grad) return fail(h, SBV_ERR_ARG, "ll or grad is NULL");
+  if (!h->prepared) return fail(h, SBV_ERR_STATE, "sbv_loglik_grad before sbv_prepare");
+  if (!y) return fail(h, SBV_ERR_ARG, "y is NULL");
+  int rc = validate_theta(h, theta);
+  if (rc) return rc;
+  const int d = h->d, P = d + 2;
+  const double nu = theta[d + 1];
+  if (!(nu == 0.5 || nu == 1.5 || nu == 2.5 || nu == 3.5))
+    return fail(h, SBV_ERR_UNSUPPORTED, "the gradient needs nu in {0.5, 1.5, 2.5, 3.5} (nu is held fixed)");
+  if (h->world > 1) return fail(h, SBV_ERR_UNSUPPORTED, "the gradient runs on one GPU (world = 1)");
+  CU(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  auto &cap = h->cap;
+  const double *yd = y;
+  if (!is_device_ptr(y)) {
+    CU(cudaMemcpyAsync(h->ybuf, y, h->n * sizeof(double), cudaMemcpyHostToDevice, st));
+    yd = h->ybuf;
+  }
+  Timer tm(h, 0);
+  CU(launch_stage_eval(yd, h->perm, h->n, h->yperm, st));
+  tm.mark("H7_stage");
+  // batches of the LPT order whose factor copies fit the budget
+  double gb = 16.0;
+  if (const char *e = getenv("SBV_GRAD_BATCH_GB")) gb = atof(e);
+  const int64_t budget = (int64_t)(gb * 1e9 / sizeof(double));
+  std::vector<int64_t> lgo(h->k_local, 0);
+  int64_t maxbatch = 0;
+  {
+    int64_t acc = 0;
+    for (int64_t it = 0; it < h->k_local; it++) {
+      const int64_t Nb = h->Nt[h->order_h[it]];
+      const int64_t sz = (Nb + 1) * Nb;
+      if (acc > 0 && acc + sz > budget) {
+        maxbatch = std::max(maxbatch, acc);
+        acc = 0;
+      }
+      lgo[h->order_h[it]] = acc;
+      acc += sz;
+    }
+    maxbatch = std::max(maxbatch, acc);
+  }
+  CU(ensure(h->Lg, std::max<int64_t>(maxbatch, 1), cap));
+  CU(ensure(h->lg_off, std::max<int64_t>(h->k_local, 1), cap));
+  CU(cudaMemcpyAsync(h->lg_off, lgo.data(), h->k_local * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  int max_b = 1;
+  for (int64_t li = 0; li < h->k_local; li++) max_b = std::max(max_b, h->Nt[li] - std::min<int32_t>(h->m, h->Nt[li]));
+  const int bpad_max = (h->max_bs + 31) & ~31;
+  int sms = 0;
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+  const int ggrid = (int)std::min<int64_t>(sms, std::max<int64_t>(h->k_local, 1));
+  CU(ensure(h->zws, (int64_t)ggrid * std::max(h->max_N, 1) * std::max(bpad_max, 32), cap));
+  CU(ensure(h->grads, std::max<int64_t>(h->k_local, 1) * P, cap));
+  CU(ensure(h->gsum, P, cap));
+  // batches: contiguous ranges [i0, i1) of the LPT order
+  int64_t i0 = 0;
+  while (i0 < h->k_local) {
+    int64_t i1 = i0 + 1;
+    while (i1 < h->k_local && lgo[h->order_h[i1]] != 0) i1++;
+    H8Problem pb{};
+    pb.Xp = h->Xperm;
+    pb.yperm = h->yperm;
+    pb.off = h->off;
+    pb.nbr = h->nbr;
+    pb.cnt = h->cnt;
+    pb.local_blocks = h->local_blocks;
+    pb.work_order = h->work_order + i0;
+    pb.k_local = i1 - i0;
+    pb.m = h->m;
+    pb.max_N = h->max_N;
+    pb.grid = (int)std::min<int64_t>(h->h8_grid, i1 - i0);
+    pb.smem = h->h8_smem;
+    pb.ws = h->ws;
+    pb.ws_per_cta = h->ws_per_cta;
+    pb.terms = h->terms;
+    pb.quads = h->quads;
+    pb.logdets = h->logdets;
+    pb.status = h->status;
+    pb.predict = 2;
+    pb.Lg = h->Lg;
+    pb.lg_off = h->lg_off;
+    CU(launch_h8_problem(pb, d, theta, h->queue, st));
+    tm.mark("H8_keep_factor");
+    GradLaunch gl{};
+    gl.Lg = h->Lg;
+    gl.lg_off = h->lg_off;
+    gl.Xp = h->Xperm;
+    gl.off = h->off;
+    gl.nbr = h->nbr;
+    gl.cnt = h->cnt;
+    gl.local_blocks = h->local_blocks;
+    gl.items = h->work_order + i0;
+    gl.n_items = i1 - i0;
+    gl.m = h->m;
+    gl.d = d;
+    gl.max_N = std::max(h->max_N, 1);
+    gl.bpad_max = std::max(bpad_max, 32);
+    gl.grid = (int)std::min<int64_t>(ggrid, i1 - i0);
+    gl.theta = theta;
+    gl.zws = h->zws;
+    gl.queue = h->queue;
+    gl.grads = h->grads;
+    CU(launch_grad(gl, st));
+    tm.mark("N3_grad");
+    if (const char *dump = getenv("SBV_GRAD_DUMP")) {  // debugging aid: Lg of the first batch + per-block grads
+      if (i0 == 0) {
+        CU(cudaStreamSynchronize(st));
+        std::vector<double> hl((size_t)maxbatch), hg((size_t)h->k_local * P);
+        CU(cudaMemcpy(hl.data(), h->Lg, hl.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(hg.data(), h->grads, hg.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        if (FILE *fp = fopen(dump, "wb")) {
+          fwrite(hl.data(), sizeof(double), hl.size(), fp);
+          fwrite(hg.data(), sizeof(double), hg.size(), fp);
+          fwrite(lgo.data(), sizeof(int64_t), lgo.size(), fp);
+          fclose(fp);
+        }
+      }
+    }
+    i0 = i1;
+  }
+  CU(launch_reduce_chunks(*h, st));
+  CU(launch_final_reduce(*h, st));
+  CU(launch_grad_sum(h->grads, h->k_local, P, h->gsum, st));
+  CU(cudaMemcpyAsync(h->result_host, h->result, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(grad, h->gsum, P * sizeof(double), cudaMemcpyDefault, st));
+  tm.mark("H9_grad_sums_d2h");
+  CU(cudaStreamSynchronize(st));
+  tm.finish();
+  if (h->result_host[4] > 0) {
+    h->err_block = (int64_t)h->result_host[5];
+    h->err_stage = (int32_t)h->result_host[6];
+    *ll = NAN;
+    return fail(h, SBV_ERR_NOT_PD, "Cholesky factorisation failed (non-positive pivot)");
+  }
+  *ll = h->result_host[0];
+  return SBV_OK;
 }
 
 int sbv_block_terms(sbv_handle h, const double *y, const double *theta, double *terms,

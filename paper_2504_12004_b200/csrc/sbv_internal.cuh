@@ -95,6 +95,13 @@ struct Ctx {
   size_t pin_cap = 0;
   unsigned int *queue = nullptr;  // work counter
   double *ws = nullptr;           // H8 per-CTA L workspaces
+  std::vector<int32_t> Nt;        // N_t = m_t + bs_t per local block (prepare)
+  std::vector<int32_t> order_h;   // LPT work order (host copy)
+  double *Lg = nullptr;           // gradient: per-block factor copies (one batch)
+  int64_t *lg_off = nullptr;      // gradient: [k_local] offsets into Lg
+  double *zws = nullptr;          // gradient: per-CTA Z scratch
+  double *grads = nullptr;        // gradient: [k_local][d+2]
+  double *gsum = nullptr;         // gradient: [d+2]
   size_t ws_per_cta = 0;
   int h8_grid = 0;
   size_t h8_smem = 0;
@@ -183,12 +190,31 @@ struct H8Problem {
   size_t ws_per_cta;
   double *terms, *quads, *logdets;
   int32_t *status;
-  int predict;                     // 1: B rows are test points Xq, outputs pmean / pvar
+  int predict;                     // 1: B rows are test points Xq, outputs pmean / pvar; 2: keep L (gradient)
+  double *Lg = nullptr;            // predict == 2: per-block factor copies
+  const int64_t *lg_off = nullptr;
   const double *Xq;
   double *pmean, *pvar;
 };
 cudaError_t launch_h8_problem(const H8Problem &pb, int d, const double *theta_host, unsigned int *queue,
                               cudaStream_t st);
+// ---- gradient (grad_kernel.cu)
+struct GradLaunch {
+  const double *Lg;
+  const int64_t *lg_off;
+  const double *Xp;
+  const int64_t *off;
+  const int32_t *nbr, *cnt, *local_blocks, *items;
+  int64_t n_items;
+  int m, d, max_N, bpad_max, grid;
+  const double *theta;  // host
+  double *zws;
+  unsigned int *queue;
+  double *grads;
+};
+size_t grad_smem_bytes(int max_N, int d);
+cudaError_t launch_grad(const GradLaunch &gl, cudaStream_t st);
+cudaError_t launch_grad_sum(const double *grads, int64_t k_local, int P, double *out, cudaStream_t st);
 cudaError_t launch_reduce_chunks(const Ctx &c, cudaStream_t st);
 cudaError_t launch_final_reduce(const Ctx &c, cudaStream_t st);
 

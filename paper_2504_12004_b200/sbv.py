@@ -45,7 +45,8 @@ EXPORTS = ["sbv_abi_version", "sbv_create", "sbv_destroy", "sbv_comm_unique_id",
            "sbv_block_terms", "sbv_num_blocks", "sbv_get_anchors", "sbv_get_blocks",
            "sbv_get_neighbors", "sbv_stats", "sbv_stage_times", "sbv_last_error",
            "sbv_predict", "sbv_get_prediction", "sbv_simulate", "sbv_set_shard",
-           "sbv_partials_size", "sbv_loglik_partials", "sbv_reduce_partials"]
+           "sbv_partials_size", "sbv_loglik_partials", "sbv_reduce_partials",
+           "sbv_loglik_grad"]
 
 
 def lib():
@@ -67,6 +68,7 @@ def lib():
                                      ctypes.POINTER(_p)]
         L.sbv_prepare.argtypes = [_p, _i64, _i32, _i32, _i32, _p, ctypes.POINTER(_p)]
         L.sbv_set_shard.argtypes = [_p, _i32, _i32]
+        L.sbv_loglik_grad.argtypes = [_p, _p, _p, ctypes.POINTER(ctypes.c_double), _p]
         L.sbv_partials_size.argtypes = [_p, ctypes.POINTER(_i64)]
         L.sbv_loglik_partials.argtypes = [_p, _p, _p, _p]
         L.sbv_reduce_partials.argtypes = [_p, _p, _p]
@@ -232,6 +234,17 @@ class Handle:
         out = ctypes.c_double(0.0)
         self._check(lib().sbv_loglik(self._h, py, th.ctypes.data_as(_p), ctypes.byref(out)))
         return out.value
+
+    def loglik_grad(self, y, theta):
+        """(ell, d ell / d (sigma2, beta_1..beta_d, tau2)) -- sbv_loglik_grad."""
+        y = _f64(y)
+        th = np.ascontiguousarray(theta, dtype=np.float64)
+        py, _k = _ptr(y)
+        out = ctypes.c_double(0.0)
+        g = np.zeros(self.d + 2)
+        self._check(lib().sbv_loglik_grad(self._h, py, th.ctypes.data_as(_p), ctypes.byref(out),
+                                          g.ctypes.data_as(_p)))
+        return out.value, g
 
     def loglik_parts(self, y, theta):
         y = _f64(y)

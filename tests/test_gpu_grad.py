@@ -1,0 +1,87 @@
+"""GPU parity of the gradient (sbv_loglik_grad) against the
+oracle's O13 (explicit inverses; pinned in tests/test_oracle_grad.py).
+
+Bar (Q28b): each component within 1e-7 of max(|g_k|, sum_t |g_t,k|)
+(the per-block gradients are sums of terms that cancel; the same guard as the
+log-likelihood's Q18), and ell bitwise equal to sbv_loglik's.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import sbv_inputs as si
+
+pytestmark = pytest.mark.gpu
+TOL_G = 1e-7
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def sbv():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2504_12004_b200 as p
+    from paper_2504_12004_b200 import build
+    build.build()
+    return p
+
+
+def _check(sbv, orc, X, y, bs, m, scale, theta, name):
+    import torch
+    h = sbv.prepare(torch.from_numpy(X).cuda(), bs, m, scale)
+    yt = torch.from_numpy(y).cuda()
+    ll, g = h.loglik_grad(yt, theta)
+    assert ll == h.loglik(yt, theta)
+    P = orc.prepare(X, bs, m, scale, 3)
+    go, gb = orc.loglik_grad(X, y, P["perm"], P["off"], P["nbr"], P["cnt"], theta, return_blocks=True)
+    base = np.maximum(np.abs(go), np.abs(gb).sum(0))
+    rel = np.abs(g - go) / base
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "parity_report.jsonl"), "a") as f:
+        f.write(json.dumps({"test": name, "max_rel_grad": float(rel.max()),
+                            "max_rel_grad_strict": float((np.abs(g - go) / np.maximum(np.abs(go), 1e-300)).max())}) + "\n")
+    assert rel.max() <= TOL_G, (rel, g, go)
+    return h, g
+
+
+@pytest.mark.parametrize("d,bs,m,nu", [
+    (5, 20, 40, 2.5),
+    (3, 10, 30, 3.5),
+    (2, 7, 13, 0.5),
+    (10, 20, 60, 1.5),   # cfg1 shape (reduced n)
+    (4, 1, 5, 2.5),      # bs = 1
+    (3, 30, 0, 2.5),     # m = 0: marginal blocks only
+])
+def test_grad_parity_small(sbv, orc, d, bs, m, nu):
+    n = 2000
+    X = si.make_X(n, d, seed=30 + d)
+    y = si.make_y(X, seed=40 + d)
+    scale = si.default_scale(d)
+    theta = si.default_theta(d, nu=nu, tau2=1e-3)
+    _check(sbv, orc, X, y, bs, m, scale, theta, f"grad_small_d{d}_bs{bs}_m{m}_nu{nu}")
+
+
+def test_grad_large_blocks_and_batches(sbv, orc, monkeypatch):
+    """N_t up to ~600 (several 32-row panels, ragged tails) and the factor
+    copies split over many batches (SBV_GRAD_BATCH_GB tiny): same gradient."""
+    n, d, bs, m = 3000, 4, 250, 300
+    X = si.make_X(n, d, seed=5)
+    y = si.make_y(X, seed=6)
+    scale = np.array([0.2, 0.3, 1.0, 2.0])
+    theta = np.array([1.3, 0.2, 0.3, 1.0, 2.0, 2.5, 1e-3])
+    h, g = _check(sbv, orc, X, y, bs, m, scale, theta, "grad_large_blocks")
+    assert h.stats()["max_N"] > 500
+    monkeypatch.setenv("SBV_GRAD_BATCH_GB", "0.002")
+    ll2, g2 = h.loglik_grad(y, theta)
+    np.testing.assert_array_equal(g2, g)
+
+
+def test_grad_rejects_general_nu(sbv):
+    X = si.make_X(500, 3, seed=1)
+    h = sbv.prepare(X, 10, 20, np.ones(3))
+    with pytest.raises(sbv.SBVError) as e:
+        h.loglik_grad(np.zeros(500), np.array([1.0, 1, 1, 1, 1.3, 1e-3]))
+    assert e.value.code == 5
