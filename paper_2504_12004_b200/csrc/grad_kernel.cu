@@ -11,8 +11,7 @@
 //   Z  = L^-T E_B            (N x b: the B columns of L^-T; Z Z^T = K^-1 - blkdiag(K_JJ^-1, 0)),
 //   v  = y'_B,  dl = Z v     (= K^-1 y - [K_JJ^-1 y_J; 0]),
 //   at = [L11^-T y'_J; 0]    (= [K_JJ^-1 y_J; 0]).
-// (Derivation in DESIGN.md §6; the oracle evaluates the same derivative the
-// plain way, explicit inverses of K and K_JJ: oracle/sbv_oracle.c O13.)
+// (Derivation in DESIGN.md §6.)
 //
 // One CTA (8 warps) per block, persistent over the batch:
 //   1. coordinates staged (centred, 1/beta scaled, as in H8) + y';
