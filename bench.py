@@ -58,49 +58,59 @@ def load_peaks():
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """SM clock and throttle reasons of one GPU, sampled DURING the timed region
+    by a background thread through NVML (every ~2 ms, so even a ~50 ms timed
+    region yields samples); nvidia-smi is the fallback."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
     def __init__(self, gpu: int):
         self.gpu = gpu
-        self.proc = None
-        self.path = os.path.join(ROOT, "gpurun_out", f"bench_clocks_{gpu}.csv")
+        self.sm, self.smax, self.reasons = [], [], set()
+        self.thread = None
+        self.stop_flag = False
+
+    def _run(self):
+        import pynvml
+        hnd = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+        smax = pynvml.nvmlDeviceGetMaxClockInfo(hnd, pynvml.NVML_CLOCK_SM)
+        while not self.stop_flag:
+            try:
+                self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(hnd, pynvml.NVML_CLOCK_SM)))
+                self.smax.append(float(smax))
+                try:
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(hnd)
+                except AttributeError:
+                    r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(hnd)
+                for nm, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(nm)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
 
     def start(self):
-        os.makedirs(os.path.dirname(self.path), exist_ok=True)
         try:
-            self.f = open(self.path, "w")
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu),
-                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.f, stderr=subprocess.DEVNULL)
-        except Exception:
-            self.proc = None
+            import threading
+            import pynvml
+            pynvml.nvmlInit()
+            self.stop_flag = False
+            self.thread = threading.Thread(target=self._run, daemon=True)
+            self.thread.start()
+        except Exception:  # noqa: BLE001
+            self.thread = None
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        self.proc.wait()
-        self.f.close()
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[4:8]):
-                if v.lower() == "active":
-                    reasons.add(nm)
+        if self.thread is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "samples": 0, "reasons": ["nvml unavailable"]}
+        self.stop_flag = True
+        self.thread.join()
+        sm = self.sm
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(smax) if smax else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+                "sm_max_mhz": max(self.smax) if self.smax else None,
+                "samples": len(sm), "source": "NVML, ~2 ms period, during the timed region",
+                "reasons": sorted(self.reasons)}
 
 
 def workload(cfg: str, ngpu: int = 1):
@@ -283,7 +293,8 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        import datetime
+        dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(seconds=300))
     if rank == 0:
         build.build()
     if world > 1:
@@ -464,48 +475,58 @@ def run_ours(args):
     if world > 1:
         stages_all = [None] * world
         dist.all_gather_object(stages_all, stages)
+    def emit():
+            evals_s = 1e3 / ms_max
+            stages_max = {k_: max(s.get(k_, 0.0) for s in stages_all) for k_ in stages}
+            stages_min = {k_: min(s.get(k_, 0.0) for s in stages_all) for k_ in stages}
+            dom = max(((k_, v) for k_, v in stages.items() if "H" in k_), key=lambda kv: kv[1])
+            h8_tf = flops_total / (h8_ms_max * 1e-3) / 1e12        # all GPUs
+            h8_tf_gpu = flops_total / world / (h8_ms_max * 1e-3) / 1e12  # per GPU (slowest rank's time)
+            roof = roofline(dom, stats, c, fp64_peak, peaks, world, h8_ms_max, flops_total, h8_bytes_total)
+            reasons = sorted({r for ckr in ck_all for r in (ckr.get("reasons") or [])})
+            sm_all = [ckr.get("sm_mhz") for ckr in ck_all if ckr.get("sm_mhz") is not None] or [None]
+            out = {
+                "metric": METRIC, "value": evals_s, "unit": "evals/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+                "higher_is_better": True, "scaling": scaling_kind(args.config), "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic", "config": config_dict(c, args.config, world),
+                "tflops_step": flops_total / (ms_max * 1e-3) / 1e12,
+                "loglik_only": {"evals_s": 1e3 / llh_ms_max, "ms": llh_ms_max,
+                                "tflops": flops_total / (llh_ms_max * 1e-3) / 1e12,
+                                "h8_ms": h8_ms_max, "h8_tflops_all_gpus": h8_tf,
+                                "h8_tflops_per_gpu": h8_tf_gpu,
+                                "h8_frac_of_fp64_peak_per_gpu": h8_tf_gpu / fp64_peak,
+                                "fp64_peak_tflops_per_gpu": fp64_peak, "flops_per_eval": flops_total},
+                "stage_ms_rank0": stages,
+                **({"stage_ms_max_over_ranks": stages_max, "stage_ms_min_over_ranks": stages_min}
+                   if world > 1 else {}),
+                "dominant_stage": dom[0],
+                "roofline": roof,
+                "roofline_knn": knn_roofline(stages_max, peaks, stats, c),
+                "e2e": {"value": 1e3 / e2e_ms_max, "unit": "evals/s",
+                        "h2d_bytes_per_step": int(n * d * 8 + n * 8), "d2h_bytes_per_step": 8 * 8},
+                "gpu_launches": launches,
+                **({"predict": pred} if pred else {}),
+                **({"gradient": grad} if grad else {}),
+                "clocks": {**ck, "reasons": reasons,
+                           **({"sm_mhz_min_over_ranks": min((x for x in sm_all if x is not None), default=None),
+                               "per_rank": ck_all} if world > 1 else {})},
+                "ll": ll,
+                "realised": stats,
+            }
+            if world == 1 and not args.no_cpu_baseline:
+                import oracle
+                oracle.build()
+                out["cpu_baseline"] = cpu_baseline_measure(c, args.config)
+            print(json.dumps(out))
+
     if rank == 0:
-        evals_s = 1e3 / ms_max
-        stages_max = {k_: max(s.get(k_, 0.0) for s in stages_all) for k_ in stages}
-        stages_min = {k_: min(s.get(k_, 0.0) for s in stages_all) for k_ in stages}
-        dom = max(((k_, v) for k_, v in stages.items() if "H" in k_), key=lambda kv: kv[1])
-        h8_tf = flops_total / (h8_ms_max * 1e-3) / 1e12        # all GPUs
-        h8_tf_gpu = flops_total / world / (h8_ms_max * 1e-3) / 1e12  # per GPU (slowest rank's time)
-        roof = roofline(dom, stats, c, fp64_peak, peaks, world, h8_ms_max, flops_total, h8_bytes_total)
-        reasons = sorted({r for ckr in ck_all for r in (ckr.get("reasons") or [])})
-        sm_all = [ckr.get("sm_mhz") for ckr in ck_all if ckr.get("sm_mhz") is not None]
-        out = {
-            "metric": METRIC, "value": evals_s, "unit": "evals/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-            "higher_is_better": True, "scaling": scaling_kind(args.config), "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic", "config": config_dict(c, args.config, world),
-            "tflops_step": flops_total / (ms_max * 1e-3) / 1e12,
-            "loglik_only": {"evals_s": 1e3 / llh_ms_max, "ms": llh_ms_max,
-                            "tflops": flops_total / (llh_ms_max * 1e-3) / 1e12,
-                            "h8_ms": h8_ms_max, "h8_tflops_all_gpus": h8_tf,
-                            "h8_tflops_per_gpu": h8_tf_gpu,
-                            "h8_frac_of_fp64_peak_per_gpu": h8_tf_gpu / fp64_peak,
-                            "fp64_peak_tflops_per_gpu": fp64_peak, "flops_per_eval": flops_total},
-            "stage_ms_rank0": stages,
-            **({"stage_ms_max_over_ranks": stages_max, "stage_ms_min_over_ranks": stages_min}
-               if world > 1 else {}),
-            "dominant_stage": dom[0],
-            "roofline": roof,
-            "e2e": {"value": 1e3 / e2e_ms_max, "unit": "evals/s",
-                    "h2d_bytes_per_step": int(n * d * 8 + n * 8), "d2h_bytes_per_step": 8 * 8},
-            "gpu_launches": launches,
-            **({"predict": pred} if pred else {}),
-            **({"gradient": grad} if grad else {}),
-            "clocks": {**ck, "reasons": reasons,
-                       **({"sm_mhz_min_over_ranks": min(sm_all), "per_rank": ck_all} if world > 1 else {})},
-            "ll": ll,
-            "realised": stats,
-        }
-        if world == 1 and not args.no_cpu_baseline:
-            import oracle
-            oracle.build()
-            out["cpu_baseline"] = cpu_baseline_measure(c, args.config)
-        print(json.dumps(out))
+        try:
+            emit()
+        except Exception as ex:  # noqa: BLE001 -- never leave the other ranks waiting at the barrier
+            import traceback
+            traceback.print_exc()
+            print(json.dumps({"metric": METRIC, "error": f"rank-0 report failed: {ex!r}"[:300]}))
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -531,6 +552,22 @@ def ncu_traffic(fname: str):
             except (KeyError, ValueError, TypeError):
                 return None
     return None
+
+
+def knn_roofline(stages, peaks, stats, c):
+    """H6 (k_knn_grid) seen against HBM: DRAM bytes of one launch (committed ncu
+    summary) over the stage's device time; the grid search is latency-bound (warp per
+    query, dependent candidate loads), so both fractions are low by construction."""
+    ms = stages.get("prep.H6_knn")
+    tr = ncu_traffic("knn_full_ncu_summary.json")
+    hbm = peaks.get("hbm_gbs", 6550.0)
+    if not ms or tr is None:
+        return None
+    ach = tr / (ms * 1e-3) / 1e9
+    return {"kernel": "k_knn_grid (exact m-NN over prefix-level grids)", "bound": "hbm",
+            "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": tr,
+            "ms": ms, "note": "latency-bound (FP64 pipe 3.3% in ncu); brute-force-equivalent pairs "
+                              f"{stats['knn_pairs']:.3g}; traffic = dram read+write of one launch (ncu)"}
 
 
 def roofline(dom, stats, c, fp64_peak, peaks, world, h8_ms, flops_total, h8_bytes_total):

@@ -2,6 +2,8 @@
 // sizing, occupancy, variant selection and launch.
 #include <stdio.h>
 
+#include <algorithm>
+
 #include "h8_kernel.cuh"
 
 namespace sbv {
@@ -28,15 +30,34 @@ static int h8_dm(int d) {
   return 0;
 }
 
-size_t h8_smem_bytes(int max_N, int d) {
+// Shared memory of one CTA: Dt/Mn, the border row ys, the flags / task list and
+// the staged coordinates of blocks with N <= h8_vs_cap(max_N, d).  The cap keeps
+// 2 CTAs per SM (2 x (dynamic + static) <= 228 KB): a larger block stages its
+// coordinates in the CTA's global scratch instead (L1-cached generic loads),
+// rather than halving the occupancy of the whole launch (measured round 2:
+// one rank of a cfg5 run with max_N ~ 800 fell to 1 CTA/SM, H8 +25%).
+static size_t h8_smem_fixed(int max_N) {
   const size_t Cp = (size_t)h8_np_max(max_N) * kPanel;
   const size_t np = h8_np_max(max_N), nch = np + 1;
   const size_t ints = 2 * np * nch + 2 * np + ((h8_max_tasks(max_N) + 1) & ~1);
-  const size_t ds = h8_dm(d) > 0 ? (size_t)h8_dm(d) : (size_t)d;
-  const size_t vs_smem = SBV_VS_GLOBAL ? 0 : (size_t)max_N * ds;  // else staged in global scratch
   return sizeof(double) * (4 * (size_t)kPanel * kDld + (kH8Threads / 32) * (size_t)kRingPerWarp +
-                           2 * SBV_MAX_D + (Cp + 8) + vs_smem) +
+                           2 * SBV_MAX_D + (Cp + 8)) +
          sizeof(int) * ((ints + 1) & ~(size_t)1);
+}
+
+int h8_vs_cap(int max_N, int d) {
+  if (SBV_VS_GLOBAL) return 0;
+  const size_t ds = h8_dm(d) > 0 ? (size_t)h8_dm(d) : (size_t)d;
+  const size_t budget = 105 * 1024;  // dynamic smem per CTA for 2 CTAs/SM (static ~4.5 KB)
+  const size_t fixed = h8_smem_fixed(max_N);
+  if (fixed >= budget) return max_N;  // cannot keep 2 CTAs/SM anyway
+  const size_t cap = (budget - fixed) / (sizeof(double) * ds);
+  return (int)std::min<size_t>((size_t)max_N, cap);
+}
+
+size_t h8_smem_bytes(int max_N, int d) {
+  const size_t ds = h8_dm(d) > 0 ? (size_t)h8_dm(d) : (size_t)d;
+  return h8_smem_fixed(max_N) + sizeof(double) * (size_t)h8_vs_cap(max_N, d) * ds;
 }
 
 // L panels of the largest block, then (ring builds) its staged coordinates
@@ -49,7 +70,7 @@ static size_t h8_l_doubles(int max_N) {
 
 size_t h8_ws_doubles(int max_N, int d) {
   const size_t ds = h8_dm(d) > 0 ? (size_t)h8_dm(d) : (size_t)d;
-  const size_t vs = SBV_VS_GLOBAL ? ((size_t)max_N * ds + 63) / 64 * 64 : 0;
+  const size_t vs = (h8_vs_cap(max_N, d) < max_N) ? ((size_t)max_N * ds + 63) / 64 * 64 : 0;
   return h8_l_doubles(max_N) + vs;
 }
 
@@ -94,6 +115,7 @@ cudaError_t launch_h8_problem(const H8Problem &pb, int d, const double *theta, u
   a.ws = pb.ws;
   a.ws_per_cta = pb.ws_per_cta;
   a.vs_off = h8_l_doubles(pb.max_N);
+  a.vs_cap = h8_vs_cap(pb.max_N, d);
   a.queue = queue;
   a.terms = pb.terms;
   a.quads = pb.quads;
