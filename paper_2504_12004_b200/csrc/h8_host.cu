@@ -30,34 +30,48 @@ static int h8_dm(int d) {
   return 0;
 }
 
-// Shared memory of one CTA: Dt/Mn, the border row ys, the flags / task list and
-// the staged coordinates of blocks with N <= h8_vs_cap(max_N, d).  The cap keeps
-// 2 CTAs per SM (2 x (dynamic + static) <= 228 KB): a larger block stages its
-// coordinates in the CTA's global scratch instead (L1-cached generic loads),
-// rather than halving the occupancy of the whole launch (measured round 2:
-// one rank of a cfg5 run with max_N ~ 800 fell to 1 CTA/SM, H8 +25%).
-static size_t h8_smem_fixed(int max_N) {
+size_t h8_smem_bytes(int max_N, int d) {
   const size_t Cp = (size_t)h8_np_max(max_N) * kPanel;
   const size_t np = h8_np_max(max_N), nch = np + 1;
   const size_t ints = 2 * np * nch + 2 * np + ((h8_max_tasks(max_N) + 1) & ~1);
+  const size_t ds = h8_dm(d) > 0 ? (size_t)h8_dm(d) : (size_t)d;
+  const size_t vs_smem = SBV_VS_GLOBAL ? 0 : (size_t)max_N * ds;  // else staged in global scratch
   return sizeof(double) * (4 * (size_t)kPanel * kDld + (kH8Threads / 32) * (size_t)kRingPerWarp +
-                           2 * SBV_MAX_D + (Cp + 8)) +
+                           2 * SBV_MAX_D + (Cp + 8) + vs_smem) +
          sizeof(int) * ((ints + 1) & ~(size_t)1);
 }
 
-int h8_vs_cap(int max_N, int d) {
-  if (SBV_VS_GLOBAL) return 0;
-  const size_t ds = h8_dm(d) > 0 ? (size_t)h8_dm(d) : (size_t)d;
-  const size_t budget = 105 * 1024;  // dynamic smem per CTA for 2 CTAs/SM (static ~4.5 KB)
-  const size_t fixed = h8_smem_fixed(max_N);
-  if (fixed >= budget) return max_N;  // cannot keep 2 CTAs/SM anyway
-  const size_t cap = (budget - fixed) / (sizeof(double) * ds);
-  return (int)std::min<size_t>((size_t)max_N, cap);
+// The split of an LPT-ordered launch (Nt_order: N of each work item, descending):
+// items with N above the 2-CTA cap go first in a launch of their own.
+void h8_split_plan(const int32_t *Nt_order, int64_t k, int d, int sms, int64_t *n_big, int *max_N_small,
+                   int *grid_small) {
+  const int cap = h8_two_cta_cap(d);
+  int64_t nb = 0;
+  while (nb < k && Nt_order[nb] > cap) nb++;
+  *n_big = (nb > 0 && nb < k) ? nb : 0;
+  *max_N_small = (nb < k) ? Nt_order[nb] : 0;
+  int per_sm = 2;
+  if (*n_big > 0) per_sm = std::max(1, h8_max_ctas_per_sm(h8_smem_bytes(*max_N_small, d), d));
+  *grid_small = (int)std::min<int64_t>((int64_t)sms * per_sm, std::max<int64_t>(k - nb, 1));
 }
 
-size_t h8_smem_bytes(int max_N, int d) {
-  const size_t ds = h8_dm(d) > 0 ? (size_t)h8_dm(d) : (size_t)d;
-  return h8_smem_fixed(max_N) + sizeof(double) * (size_t)h8_vs_cap(max_N, d) * ds;
+// Largest N whose shared memory still leaves room for 2 CTAs per SM (dynamic +
+// static <= ~113 KB).  A launch with larger blocks is split (launch_h8_problem):
+// those blocks, first in the LPT order, run in their own launch sized for
+// them (1 CTA/SM), the rest at 2 CTAs/SM -- instead of running the whole
+// launch at 1 CTA/SM (measured round 2: one rank of a cfg5 run with max_N ~ 800
+// lost 25% in H8).
+int h8_two_cta_cap(int d) {
+  const size_t budget = 105 * 1024;
+  int lo = 1, hi = 4096;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) / 2;
+    if (h8_smem_bytes(mid, d) <= budget)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
 }
 
 // L panels of the largest block, then (ring builds) its staged coordinates
@@ -70,7 +84,7 @@ static size_t h8_l_doubles(int max_N) {
 
 size_t h8_ws_doubles(int max_N, int d) {
   const size_t ds = h8_dm(d) > 0 ? (size_t)h8_dm(d) : (size_t)d;
-  const size_t vs = (h8_vs_cap(max_N, d) < max_N) ? ((size_t)max_N * ds + 63) / 64 * 64 : 0;
+  const size_t vs = SBV_VS_GLOBAL ? ((size_t)max_N * ds + 63) / 64 * 64 : 0;
   return h8_l_doubles(max_N) + vs;
 }
 
@@ -115,7 +129,6 @@ cudaError_t launch_h8_problem(const H8Problem &pb, int d, const double *theta, u
   a.ws = pb.ws;
   a.ws_per_cta = pb.ws_per_cta;
   a.vs_off = h8_l_doubles(pb.max_N);
-  a.vs_cap = h8_vs_cap(pb.max_N, d);
   a.queue = queue;
   a.terms = pb.terms;
   a.quads = pb.quads;
@@ -152,8 +165,27 @@ cudaError_t launch_h8_problem(const H8Problem &pb, int d, const double *theta, u
 #endif
   {
     const H8Fn f = pick(nu, d, pb.predict);
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pb.smem);
-    f<<<pb.grid, kH8Threads, pb.smem, st>>>(a);
+    if (pb.n_big > 0 && pb.n_big < pb.k_local) {
+      // split launch (h8_two_cta_cap): the n_big largest blocks (first in the
+      // LPT order) with shared memory sized for them, then the rest at 2 CTAs/SM
+      H8Args ab = a;
+      ab.k_local = pb.n_big;
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pb.smem);
+      f<<<(int)std::min<int64_t>(pb.grid, pb.n_big), kH8Threads, pb.smem, st>>>(ab);
+      e = cudaMemsetAsync(queue, 0, sizeof(unsigned int), st);
+      if (e) return e;
+      H8Args as = a;
+      as.work_order = pb.work_order + pb.n_big;
+      as.k_local = pb.k_local - pb.n_big;
+      as.np_max = h8_np_max(pb.max_N_small);
+      as.max_tasks = h8_max_tasks(pb.max_N_small);
+      const size_t sm2 = h8_smem_bytes(pb.max_N_small, d);
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+      f<<<(int)std::min<int64_t>(pb.grid_small, as.k_local), kH8Threads, sm2, st>>>(as);
+    } else {
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pb.smem);
+      f<<<pb.grid, kH8Threads, pb.smem, st>>>(a);
+    }
   }
 #if SBV_TRACE
   if (const char *out = getenv("SBV_TRACE_OUT")) {
@@ -192,6 +224,9 @@ cudaError_t launch_h8(const Ctx &c, const double *theta, cudaStream_t st) {
   pb.quads = c.quads;
   pb.logdets = c.logdets;
   pb.status = c.status;
+  pb.n_big = c.h8_n_big;
+  pb.max_N_small = c.h8_max_N_small;
+  pb.grid_small = c.h8_grid_small;
   return launch_h8_problem(pb, c.d, theta, c.queue, st);
 }
 

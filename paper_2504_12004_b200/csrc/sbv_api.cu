@@ -744,8 +744,13 @@ int prepare_impl(sbv_ctx *h, const double *X, int64_t n, int32_t d, int32_t bs, 
   int per_sm = h->occ_per_sm;
   if (per_sm < 1) per_sm = 1;
   h->h8_grid = (int)std::min<int64_t>((int64_t)sms * per_sm, std::max<int64_t>(h->k_local, 1));
+  {
+    std::vector<int32_t> No(h->k_local);
+    for (int64_t it = 0; it < h->k_local; it++) No[it] = Nt[order[it]];
+    h8_split_plan(No.data(), h->k_local, d, sms, &h->h8_n_big, &h->h8_max_N_small, &h->h8_grid_small);
+  }
   h->ws_per_cta = h8_ws_doubles(std::max(h->max_N, 1), d);
-  CU(ensure(h->ws, (size_t)h->h8_grid * h->ws_per_cta, unused));
+  CU(ensure(h->ws, (size_t)std::max(h->h8_grid, h->h8_grid_small) * h->ws_per_cta, unused));
   // no trailing host sync: everything above is stream-ordered before the
   // first sbv_loglik; the pinned staging is guarded by ev_pin
   tm.mark("meta");
@@ -949,6 +954,9 @@ int sbv_loglik_grad(sbv_handle h, const double *y, const double *theta, double *
     pb.logdets = h->logdets;
     pb.status = h->status;
     pb.predict = 2;
+    pb.n_big = std::max<int64_t>(0, std::min<int64_t>(h->h8_n_big, i1) - i0);
+    pb.max_N_small = h->h8_max_N_small;
+    pb.grid_small = h->h8_grid_small;
     pb.Lg = h->Lg;
     pb.lg_off = h->lg_off;
     CU(launch_h8_problem(pb, d, theta, h->queue, st));
@@ -1231,8 +1239,15 @@ int sbv_predict(sbv_handle h, const double *Xs, int64_t ns, int32_t bs_pred, int
     return fail(h, SBV_ERR_UNSUPPORTED, "test block + neighbour set too large for shared memory staging");
   const int per_sm = std::max(1, h8_max_ctas_per_sm(smem, d));
   const int grid = (int)std::min<int64_t>((int64_t)sms * per_sm, ks);
+  int64_t q_n_big = 0;
+  int q_max_N_small = 0, q_grid_small = 0;
+  {
+    std::vector<int32_t> No(ks);
+    for (int64_t it = 0; it < ks; it++) No[it] = Nt[order[it]];
+    h8_split_plan(No.data(), ks, d, sms, &q_n_big, &q_max_N_small, &q_grid_small);
+  }
   const size_t ws_per_cta = h8_ws_doubles(maxN, d);
-  CU(ensure(h->ws, (size_t)grid * ws_per_cta, cap));
+  CU(ensure(h->ws, (size_t)std::max(grid, q_grid_small) * ws_per_cta, cap));
   CU(ensure(h->q_mean, ns, cap));
   CU(ensure(h->q_var, ns, cap));
   CU(ensure(h->q_terms, ks, cap));
@@ -1260,6 +1275,9 @@ int sbv_predict(sbv_handle h, const double *Xs, int64_t ns, int32_t bs_pred, int
   pb.logdets = h->q_logdets;
   pb.status = h->q_status;
   pb.predict = 1;
+  pb.n_big = q_n_big;
+  pb.max_N_small = q_max_N_small;
+  pb.grid_small = q_grid_small;
   pb.Xq = h->Xqp;
   pb.pmean = h->q_mean;
   pb.pvar = h->q_var;

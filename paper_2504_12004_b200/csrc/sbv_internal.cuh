@@ -104,6 +104,8 @@ struct Ctx {
   double *gsum = nullptr;         // gradient: [d+2]
   size_t ws_per_cta = 0;
   int h8_grid = 0;
+  int64_t h8_n_big = 0;           // split H8 launch (h8_split_plan)
+  int h8_max_N_small = 0, h8_grid_small = 0;
   size_t h8_smem = 0;
   size_t occ_smem = 0;  // cached occupancy query
   int occ_per_sm = 0;
@@ -174,6 +176,9 @@ cudaError_t launch_knn(const double *Sperm, const int32_t *perm, const int64_t *
 cudaError_t launch_stage_eval(const double *y, const int32_t *perm, int64_t n, double *yperm,
                               cudaStream_t st);
 size_t h8_smem_bytes(int max_N, int d);
+int h8_two_cta_cap(int d);
+void h8_split_plan(const int32_t *Nt_order, int64_t k, int d, int sms, int64_t *n_big, int *max_N_small,
+                   int *grid_small);
 size_t h8_ws_doubles(int max_N, int d);
 int h8_max_ctas_per_sm(size_t smem, int d);
 cudaError_t launch_h8(const Ctx &c, const double *theta_host, cudaStream_t st);
@@ -191,6 +196,8 @@ struct H8Problem {
   double *terms, *quads, *logdets;
   int32_t *status;
   int predict;                     // 1: B rows are test points Xq, outputs pmean / pvar; 2: keep L (gradient)
+  int64_t n_big = 0;               // split launch: the first n_big work items (N > 2-CTA cap) alone
+  int max_N_small = 0, grid_small = 0;
   double *Lg = nullptr;            // predict == 2: per-block factor copies
   const int64_t *lg_off = nullptr;
   const double *Xq;
