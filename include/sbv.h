@@ -153,6 +153,18 @@ int sbv_loglik(sbv_handle h, const double *y, const double *theta, double *ll);
  * for nu outside {0.5, 1.5, 2.5, 3.5} or world > 1. */
 int sbv_loglik_grad(sbv_handle h, const double *y, const double *theta, double *ll, double *grad);
 
+/* CUDA-graph replay of sbv_loglik (the latency case, cfg1: P:752 names
+ * per-call overhead as what limits small problems).  enable = 1: on one GPU
+ * (world 1) with a DEVICE y and profiling off, sbv_loglik / sbv_loglik_parts
+ * run H7 -> H8 -> H9 -> the 64-byte result copy as one graph launch, captured
+ * on the first call for a given (y pointer, nu) after each prepare and
+ * replayed afterwards; theta travels through a pinned host -> device copy
+ * node, so a new theta needs no re-capture.  Same kernels, bit-identical
+ * results; any other call shape takes the ordinary stream path.  The caller
+ * must not free y while the handle may replay the graph on it.
+ * Errors: SBV_ERR_ARG (enable not 0/1). */
+int sbv_set_graph(sbv_handle h, int32_t enable);
+
 /* As sbv_loglik, plus parts[0..3] = {ell, sum quad, sum logdet, #points}
  * (host double[4], may be NULL). */
 int sbv_loglik_parts(sbv_handle h, const double *y, const double *theta, double *parts);

@@ -14,16 +14,20 @@
 // (Derivation in DESIGN.md §6.)
 //
 // One CTA (8 warps) per block, persistent over the batch:
-//   1. coordinates staged (centred, 1/beta scaled, as in H8) + y';
-//   2. at by an axpy back substitution with L11 rows (one warp);
-//   3. Z by a blocked backward TRSM, 32-row panels from the bottom, each warp
-//      owning 32-column slices of Z: DMMA GEMM of the panel's rows against
-//      the rows below, then a 32x32 back substitution (lane = column);
-//   4. dl = Z v;
-//   5. every 32x32 lower tile (I >= J) of the N x N index space: W = Z_I Z_J^T
+//   1. coordinates staged (centred, 1/beta scaled, as in H8), y', 1/L_ii;
+//   2. Z and at together by ONE blocked backward TRSM, L^-T [E_B | 0 | y'_J; 0]
+//      (at = L^-T [y'_J; 0] is the extra right-hand side in column cz4 =
+//      round4(b), outside the W contraction), 32-row panels from the bottom,
+//      each warp owning kGSW-column slices: DMMA GEMM of the panel's rows
+//      against the rows below (kGPF-deep register prefetch of the L2
+//      operands), then a 32x32 back substitution (lane = column) against L_pp
+//      staged in shared memory;
+//   3. dl = Z v;
+//   4. every 32x32 lower tile (I >= J) of the N x N index space: W = Z_I Z_J^T
 //      on DMMA, then per entry G_ij and the covariance derivatives generated
-//      on the fly (Eq.5-6 differentiated), accumulated per parameter;
-//   6. fixed-order reductions: lanes -> warps -> the block's gradient.
+//      on the fly (Eq.5-6 differentiated; e^{-r} by the 256-entry table of
+//      H8, f'(r)/r in closed form), accumulated per parameter;
+//   5. fixed-order reductions: lanes -> warps -> the block's gradient.
 #include <math.h>
 
 #include "h8_kernel.cuh"
@@ -50,24 +54,62 @@ struct GradArgs {
   double *grads;             // [k_local][P]
 };
 
-// f(r) and f'(r) of the half-integer closed forms (sigma2 = 1), NU2 = 2 nu
+#ifndef SBV_GRAD_SW
+#define SBV_GRAD_SW 32  // Z columns per TRSM slice (one warp each)
+#endif
+#ifndef SBV_GRAD_PF
+#define SBV_GRAD_PF 2  // k-steps of register prefetch in the DMMA loops
+#endif
+constexpr int kGSW = SBV_GRAD_SW, kGPF = SBV_GRAD_PF, kGW = kGThreads / 32;
+
+// f(r) and h(r) = f'(r)/r of the half-integer closed forms (sigma2 = 1),
+// NU2 = 2 nu, e = e^{-r}, ri = 1/r (used by nu = 1/2 only)
 template <int NU2>
-__device__ __forceinline__ double matern_f_df(double r, double &df) {
-  const double e = exp(-r);
+__device__ __forceinline__ double matern_f_h(double r, double e, double ri, double &h) {
   if (NU2 == 1) {
-    df = -e;
+    h = -e * ri;
     return e;
   }
   if (NU2 == 3) {
-    df = -r * e;
+    h = -e;
     return (1.0 + r) * e;
   }
   if (NU2 == 5) {
-    df = -(r * (1.0 / 3.0)) * (1.0 + r) * e;
+    h = -(1.0 / 3.0) * (1.0 + r) * e;
     return fma(r, fma(r, 1.0 / 3.0, 1.0), 1.0) * e;
   }
-  df = -(r * (1.0 / 15.0)) * fma(r, r + 3.0, 3.0) * e;
+  h = -(1.0 / 15.0) * fma(r, r + 3.0, 3.0) * e;
   return fma(r, fma(r, fma(r, 1.0 / 15.0, 2.0 / 5.0), 1.0), 1.0) * e;
+}
+
+// acc[4][NCT] (+)= A B^T over k in [kb, ke) in steps of 4: la(k, A[4]) and
+// lb(k, B[NCT]) load the m8n8k4 fragments of one k-step (zero beyond the
+// matrix); kGPF k-steps of loads in flight
+template <int NCT, class LA, class LB>
+__device__ __forceinline__ void gemm_pf(double (&acc)[4][NCT][2], int kb, int ke, LA la, LB lb) {
+  double af[kGPF][4], bf[kGPF][NCT];
+#pragma unroll
+  for (int s = 0; s < kGPF; s++)
+    if (kb + 4 * s < ke) {
+      la(kb + 4 * s, af[s]);
+      lb(kb + 4 * s, bf[s]);
+    }
+  for (int k0 = kb; k0 < ke; k0 += 4 * kGPF) {
+#pragma unroll
+    for (int s = 0; s < kGPF; s++) {
+      const int k = k0 + 4 * s;
+      if (k < ke) {
+#pragma unroll
+        for (int rt = 0; rt < 4; rt++)
+#pragma unroll
+          for (int ct = 0; ct < NCT; ct++) dmma(acc[rt][ct][0], acc[rt][ct][1], af[s][rt], bf[s][ct]);
+        if (k + 4 * kGPF < ke) {
+          la(k + 4 * kGPF, af[s]);
+          lb(k + 4 * kGPF, bf[s]);
+        }
+      }
+    }
+  }
 }
 
 // DM > 0: coordinates staged with the padded row stride DM (d <= DM, zero
@@ -76,6 +118,7 @@ template <int NU2, int DM>
 __global__ void __launch_bounds__(kGThreads, 1) k_grad(GradArgs a) {
   extern __shared__ double gsm[];
   __shared__ int s_item;
+  __shared__ double s_etab[256];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int d = a.d, P = a.P;
@@ -85,10 +128,12 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grad(GradArgs a) {
   double *yp = vs + (size_t)Nmax * DS;    // y' (N)
   double *at = yp + Nmax;                 // at (N; zero on B)
   double *dl = at + Nmax;                 // dl (N)
-  double *red = dl + Nmax;                // 8 warps x P partial gradients
-  double *xref = red + 8 * P;             // d
-  double *Wt = xref + SBV_MAX_D + warp * 32 * 33;  // this warp's 32 x 32 W tile (row-major, ld 33)
+  double *rinv = dl + Nmax;               // 1 / L_ii (N)
+  double *red = rinv + Nmax;              // 8 warps x P partial gradients
+  double *xref = red + kGW * P;           // d
+  double *Wt = xref + SBV_MAX_D + warp * 32 * 33;  // this warp's 32 x 32 tile (row-major, ld 33)
   double *Z = a.zws + (size_t)blockIdx.x * Nmax * a.bpad_max;
+  for (int j = tid; j < 256; j += kGThreads) s_etab[j] = exp2(j / 256.0);
 
   for (;;) {
     if (tid == 0) s_item = (int)atomicAdd(a.queue, 1u);
@@ -101,9 +146,11 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grad(GradArgs a) {
     const int64_t b0 = a.off[t];
     const int bb = (int)(a.off[t + 1] - b0);
     const int N = mt + bb;
-    const int bpad = (bb + 31) & ~31;
+    const int cz4 = (bb + 3) & ~3;                 // W contraction columns (zero beyond bb)
+    const int nsl = (cz4 + 1 + kGSW - 1) / kGSW;   // slices incl. the at column cz4
+    const int bpad = nsl * kGSW;                   // Z row stride
     const double *L = a.Lg + a.lg_off[li];  // (N+1) x N, row i at L + i N
-    // ---- 1. coordinates (centred on the block's first member, 1/beta) and y'
+    // ---- 1. coordinates (centred on the block's first member, 1/beta), y', 1/L_ii
     for (int j = tid; j < d; j += kGThreads) xref[j] = a.Xp[b0 * d + j];
     __syncthreads();
     for (int e = tid; e < N * DS; e += kGThreads) {
@@ -113,110 +160,88 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grad(GradArgs a) {
     }
     for (int i = tid; i < N; i += kGThreads) {
       yp[i] = L[(size_t)N * N + i];
-      at[i] = i < mt ? yp[i] : 0.0;
+      rinv[i] = 1.0 / L[(size_t)i * N + i];
     }
     __syncthreads();
-    // ---- 2 + 3. Z = L^-T E_B in slices of 32 columns of B (one warp per slice,
-    // bottom-up over 32-row panels); at_J = L11^-T y'_J by the first warp
-    // that has one slice fewer than the others (axpy form over the rows of L11).
-    // (8-column slices keep more warps busy but re-read L per slice: measured
-    // slower, 91 vs 65 ms at cfg2.)
-    constexpr int kSW = 32;
+    // ---- 2. [Z | at] = L^-T [E_B | y'_J; 0], slices of kGSW columns, one warp
+    // each, bottom-up over 32-row panels
+    constexpr int NCT = kGSW / 8;
     const int NPn = (N + 31) >> 5;
-    const int nsl = (bb + kSW - 1) / kSW;
-    const int w2 = nsl % (kGThreads / 32);
-    for (int task = warp; task < nsl + (kGThreads / 32); task += kGThreads / 32) {
-      if (task >= nsl) {
-        if (warp != w2) continue;
-        for (int i = mt - 1; i >= 0; i--) {
-          const double ai = at[i] / L[(size_t)i * N + i];
-          __syncwarp();
-          if (lane == 0) at[i] = ai;
-          for (int k = lane; k < i; k += 32) at[k] = fma(-L[(size_t)i * N + k], ai, at[k]);
-          __syncwarp();
-        }
-        continue;
-      }
-      const int sl = task;
+    for (int sl = warp; sl < nsl; sl += kGW) {
+      const int cb = sl * kGSW;
       for (int p = NPn - 1; p >= 0; p--) {
         const int r0 = p * 32;
-        double acc[4][4][2];
-        // E_B[panel rows, slice columns]: 1 at (m + c, c)
+        double acc[4][NCT][2];
+        // right-hand sides at the panel rows: 1 at (mt + c, c) for c < bb,
+        // y'_J in column cz4
 #pragma unroll
         for (int rt = 0; rt < 4; rt++)
 #pragma unroll
-          for (int ct = 0; ct < 4; ct++)
+          for (int ct = 0; ct < NCT; ct++)
 #pragma unroll
             for (int i = 0; i < 2; i++) {
-              const int row = r0 + rt * 8 + g, col = sl * kSW + ct * 8 + 2 * q + i;
-              acc[rt][ct][i] = (col < bb && row == mt + col) ? 1.0 : 0.0;
+              const int row = r0 + rt * 8 + g, col = cb + ct * 8 + 2 * q + i;
+              acc[rt][ct][i] = col < bb ? (row == mt + col ? 1.0 : 0.0) : (col == cz4 && row < mt ? yp[row] : 0.0);
             }
         // acc -= L[k, panel cols]^T Z[k, slice cols] over rows k >= r0 + 32
-        // (operands of the next k-step loaded one step ahead)
-        {
-          double af[4], bf[4], an[4], bn[4];
-          auto ldz = [&](int k0, double (&A)[4], double (&B)[4]) {
-            const int kr = k0 + q;
+        gemm_pf<NCT>(
+            acc, r0 + 32, N,
+            [&](int k0, double (&A)[4]) {
+              const int kr = k0 + q;
 #pragma unroll
-            for (int rt = 0; rt < 4; rt++) A[rt] = (kr < N) ? -L[(size_t)kr * N + r0 + rt * 8 + g] : 0.0;
+              for (int rt = 0; rt < 4; rt++) A[rt] = (kr < N) ? -L[(size_t)kr * N + r0 + rt * 8 + g] : 0.0;
+            },
+            [&](int k0, double (&B)[NCT]) {
+              const int kr = k0 + q;
 #pragma unroll
-            for (int ct = 0; ct < 4; ct++) B[ct] = (kr < N) ? Z[(size_t)kr * bpad + sl * kSW + ct * 8 + g] : 0.0;
-          };
-          if (r0 + 32 < N) ldz(r0 + 32, af, bf);
-          for (int k0 = r0 + 32; k0 < N; k0 += 4) {
-            if (k0 + 4 < N) ldz(k0 + 4, an, bn);
-#pragma unroll
-            for (int rt = 0; rt < 4; rt++)
-#pragma unroll
-              for (int ct = 0; ct < 4; ct++) dmma(acc[rt][ct][0], acc[rt][ct][1], af[rt], bf[ct]);
-#pragma unroll
-            for (int x = 0; x < 4; x++) {
-              af[x] = an[x];
-              bf[x] = bn[x];
-            }
-          }
-        }
-        // 32x32 back substitution with L_pp^T; lane = column: park acc in
-        // this panel's rows of the slice, then solve in registers
+              for (int ct = 0; ct < NCT; ct++) B[ct] = (kr < N) ? Z[(size_t)kr * bpad + cb + ct * 8 + g] : 0.0;
+            });
+        // park acc in this panel's rows of the slice; stage L_pp (lower) in Wt
 #pragma unroll
         for (int rt = 0; rt < 4; rt++)
 #pragma unroll
-          for (int ct = 0; ct < 4; ct++)
+          for (int ct = 0; ct < NCT; ct++)
 #pragma unroll
             for (int i = 0; i < 2; i++) {
-              const int row = r0 + rt * 8 + g, col = sl * kSW + ct * 8 + 2 * q + i;
+              const int row = r0 + rt * 8 + g, col = cb + ct * 8 + 2 * q + i;
               if (row < N) Z[(size_t)row * bpad + col] = acc[rt][ct][i];
             }
-        __syncwarp();
         const int nr = min(32, N - r0);
-        double z[32];
-#pragma unroll
-        for (int i = 0; i < 32; i++) z[i] = i < nr ? Z[(size_t)(r0 + i) * bpad + sl * kSW + lane] : 0.0;
-#pragma unroll
-        for (int i = 31; i >= 0; i--) {
-          if (i < nr) {
-            const double *Lr = L + (size_t)(r0 + i) * N + r0;
-            z[i] = z[i] / Lr[i];
-#pragma unroll
-            for (int k = 0; k < i; k++) z[k] = fma(-Lr[k], z[i], z[k]);
-          }
-        }
-        __syncwarp();
-#pragma unroll
+#pragma unroll 8
         for (int i = 0; i < 32; i++)
-          if (i < nr) Z[(size_t)(r0 + i) * bpad + sl * kSW + lane] = z[i];
+          Wt[i * 33 + lane] = (i < nr && lane <= i) ? L[(size_t)(r0 + i) * N + r0 + lane] : 0.0;
+        __syncwarp();
+        // 32 x 32 back substitution with L_pp^T, lane = column
+        if (lane < kGSW) {
+          double z[32];
+#pragma unroll
+          for (int i = 0; i < 32; i++) z[i] = i < nr ? Z[(size_t)(r0 + i) * bpad + cb + lane] : 0.0;
+#pragma unroll
+          for (int i = 31; i >= 0; i--) {
+            if (i < nr) {
+              z[i] *= rinv[r0 + i];
+#pragma unroll
+              for (int k = 0; k < i; k++) z[k] = fma(-Wt[i * 33 + k], z[i], z[k]);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 32; i++)
+            if (i < nr) Z[(size_t)(r0 + i) * bpad + cb + lane] = z[i];
+        }
         __syncwarp();
       }
     }
     __syncthreads();
-    // ---- 4. dl = Z v, v = y'_B
+    // ---- 3. dl = Z v (v = y'_B); at = column cz4
     for (int i = tid; i < N; i += kGThreads) {
+      const double *zr = Z + (size_t)i * bpad;
       double s = 0.0;
-      for (int c = 0; c < bb; c++) s = fma(Z[(size_t)i * bpad + c], yp[mt + c], s);
+      for (int c = 0; c < bb; c++) s = fma(zr[c], yp[mt + c], s);
       dl[i] = s;
+      at[i] = zr[cz4];
     }
     __syncthreads();
-    // ---- 5. lower tiles of G = at dl^T + dl at^T + dl dl^T - Z Z^T against dK:
+    // ---- 4. lower tiles of G = at dl^T + dl at^T + dl dl^T - Z Z^T against dK:
     // W tile on DMMA -> this warp's shared tile -> lane = column j, loop over
     // the tile's rows i (the column's coordinates stay in registers)
     constexpr int GK = DM > 0 ? DM + 2 : 2 + SBV_MAX_D;
@@ -224,7 +249,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grad(GradArgs a) {
 #pragma unroll
     for (int k = 0; k < GK; k++) gk[k] = 0.0;
     const int ntile = NPn * (NPn + 1) / 2;
-    for (int tI = warp; tI < ntile; tI += kGThreads / 32) {
+    for (int tI = warp; tI < ntile; tI += kGW) {
       int I = 0;
       while ((I + 1) * (I + 2) / 2 <= tI) I++;
       const int J = tI - I * (I + 1) / 2;
@@ -233,33 +258,22 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grad(GradArgs a) {
       for (int rt = 0; rt < 4; rt++)
 #pragma unroll
         for (int ct = 0; ct < 4; ct++) acc[rt][ct][0] = acc[rt][ct][1] = 0.0;
-      double af[4], bf[4], an[4], bn[4];
-      auto ldw = [&](int c0, double (&A)[4], double (&B)[4]) {
+      gemm_pf<4>(
+          acc, 0, cz4,
+          [&](int c0, double (&A)[4]) {
 #pragma unroll
-        for (int rt = 0; rt < 4; rt++) {
-          const int row = I * 32 + rt * 8 + g;
-          A[rt] = row < N ? Z[(size_t)row * bpad + c0 + q] : 0.0;
-        }
+            for (int rt = 0; rt < 4; rt++) {
+              const int row = I * 32 + rt * 8 + g;
+              A[rt] = row < N ? Z[(size_t)row * bpad + c0 + q] : 0.0;
+            }
+          },
+          [&](int c0, double (&B)[4]) {
 #pragma unroll
-        for (int ct = 0; ct < 4; ct++) {
-          const int row = J * 32 + ct * 8 + g;
-          B[ct] = row < N ? Z[(size_t)row * bpad + c0 + q] : 0.0;
-        }
-      };
-      const int cz = nsl * kSW;  // Z columns written by step 3 (zero beyond bb)
-      ldw(0, af, bf);
-      for (int c0 = 0; c0 < cz; c0 += 4) {
-        if (c0 + 4 < cz) ldw(c0 + 4, an, bn);
-#pragma unroll
-        for (int rt = 0; rt < 4; rt++)
-#pragma unroll
-          for (int ct = 0; ct < 4; ct++) dmma(acc[rt][ct][0], acc[rt][ct][1], af[rt], bf[ct]);
-#pragma unroll
-        for (int x = 0; x < 4; x++) {
-          af[x] = an[x];
-          bf[x] = bn[x];
-        }
-      }
+            for (int ct = 0; ct < 4; ct++) {
+              const int row = J * 32 + ct * 8 + g;
+              B[ct] = row < N ? Z[(size_t)row * bpad + c0 + q] : 0.0;
+            }
+          });
 #pragma unroll
       for (int rt = 0; rt < 4; rt++)
 #pragma unroll
@@ -270,49 +284,62 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grad(GradArgs a) {
       __syncwarp();
       const int j = J * 32 + lane;
       if (j < N) {
-        double xc[DM > 0 ? DM : 1];
+        const double atj = at[j], dlj = dl[j];
+        const int i0 = I * 32, i1 = min(N, I * 32 + 32);
         if constexpr (DM > 0) {
+          double xc[DM];
 #pragma unroll
           for (int jj = 0; jj < DM; jj++) xc[jj] = vs[(size_t)j * DM + jj];
-        }
-        const double atj = at[j], dlj = dl[j];
-        const int i1 = min(N, I * 32 + 32);
+          // rows in pairs (two independent dependency chains); rows above the
+          // diagonal (i < j) and past the block get weight 0
 #pragma unroll 1
-        for (int i = max(I * 32, j); i < i1; i++) {
-          const double G = fma(at[i], dlj, fma(dl[i], atj, fma(dl[i], dlj, -Wt[(i - I * 32) * 33 + lane])));
-          const double wg = (i == j) ? 0.5 * G : G;  // 1/2 sum over the full symmetric matrix
-          if constexpr (DM > 0) {
-            double u2[DM];
-            double s2 = 0.0;
+          for (int ib = i0; ib < i1; ib += 2) {
 #pragma unroll
-            for (int jj = 0; jj < DM; jj++) {
-              const double u = vs[(size_t)i * DM + jj] - xc[jj];
-              u2[jj] = u * u;
-              s2 += u2[jj];
+            for (int h2 = 0; h2 < 2; h2++) {
+              const int i = min(ib + h2, i1 - 1);
+              const double G = fma(at[i], dlj, fma(dl[i], atj, fma(dl[i], dlj, -Wt[(i - i0) * 33 + lane])));
+              const double wg = (ib + h2 >= i1 || i < j) ? 0.0 : (i == j ? 0.5 * G : G);  // 1/2 sum over the symmetric matrix
+              double u2[DM];
+              double s2 = 0.0;
+#pragma unroll
+              for (int jj = 0; jj < DM; jj++) {
+                const double u = vs[(size_t)i * DM + jj] - xc[jj];
+                u2[jj] = u * u;
+                s2 += u2[jj];
+              }
+              const double ri = rsqrt_pos(fmax(s2, 1e-300));
+              const double r = s2 * ri;
+              const double e = neg_sigma2_exp_neg(r, s_etab);  // table holds 2^{j/256}: e = e^{-r}
+              double hr;
+              const double f = matern_f_h<NU2>(r, e, ri, hr);
+              gk[0] = fma(wg, f, gk[0]);
+              const double coef = s2 > 0.0 ? -a.sigma2 * hr * wg : 0.0;  // dK/dbeta_j = coef u_j^2 / beta_j
+#pragma unroll
+              for (int jj = 0; jj < DM; jj++) gk[1 + jj] = fma(coef, u2[jj], gk[1 + jj]);
+              if (i == j && ib + h2 < i1) gk[DM + 1] += wg;
             }
-            const double r = sqrt(s2);
-            double df;
-            const double f = matern_f_df<NU2>(r, df);
-            gk[0] = fma(wg, f, gk[0]);
-            const double coef = r > 0.0 ? -a.sigma2 * df / r * wg : 0.0;  // dK/dbeta_j = coef u_j^2 / beta_j
-#pragma unroll
-            for (int jj = 0; jj < DM; jj++) gk[1 + jj] = fma(coef * a.inv_beta[jj], u2[jj], gk[1 + jj]);
-            if (i == j) gk[DM + 1] += wg;
-          } else {
+          }
+        } else {
+#pragma unroll 1
+          for (int i = max(i0, j); i < i1; i++) {
+            const double G = fma(at[i], dlj, fma(dl[i], atj, fma(dl[i], dlj, -Wt[(i - i0) * 33 + lane])));
+            const double wg = (i == j) ? 0.5 * G : G;
             const double *xi = vs + (size_t)i * d, *xj = vs + (size_t)j * d;
             double s2 = 0.0;
             for (int jj = 0; jj < d; jj++) {
               const double u = xi[jj] - xj[jj];
               s2 = fma(u, u, s2);
             }
-            const double r = sqrt(s2);
-            double df;
-            const double f = matern_f_df<NU2>(r, df);
+            const double ri = rsqrt_pos(fmax(s2, 1e-300));
+            const double r = s2 * ri;
+            const double e = neg_sigma2_exp_neg(r, s_etab);
+            double hr;
+            const double f = matern_f_h<NU2>(r, e, ri, hr);
             gk[0] = fma(wg, f, gk[0]);
-            const double coef = r > 0.0 ? -a.sigma2 * df / r * wg : 0.0;
+            const double coef = s2 > 0.0 ? -a.sigma2 * hr * wg : 0.0;
             for (int jj = 0; jj < d; jj++) {
               const double u = xi[jj] - xj[jj];
-              gk[1 + jj] = fma(coef * a.inv_beta[jj], u * u, gk[1 + jj]);
+              gk[1 + jj] = fma(coef, u * u, gk[1 + jj]);
             }
             if (i == j) gk[d + 1] += wg;
           }
@@ -320,9 +347,9 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grad(GradArgs a) {
       }
       __syncwarp();
     }
-    // gradient slots: sigma2 | beta_1..beta_d | tau2 (DM > 0: tau2 is slot DM + 1,
-    // slots d+1..DM belong to zero-padded dimensions)
-    // ---- 6. fixed-order reductions: lanes (xor tree), warps (in order)
+    // gradient slots: sigma2 | beta_1..beta_d (times 1/beta_j here) | tau2
+    // (DM > 0: tau2 is slot DM + 1, slots d+1..DM belong to zero-padded dimensions)
+    // ---- 5. fixed-order reductions: lanes (xor tree), warps (in order)
 #pragma unroll
     for (int kk = 0; kk < GK; kk++) {
       const int dst = (DM > 0 && kk == DM + 1) ? P - 1 : kk;
@@ -330,12 +357,13 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grad(GradArgs a) {
       double v = gk[kk];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (kk >= 1 && kk <= d) v *= a.inv_beta[kk - 1];
       if (lane == 0) red[warp * P + dst] = v;
     }
     __syncthreads();
     for (int k = tid; k < P; k += kGThreads) {
       double v = 0.0;
-      for (int w = 0; w < kGThreads / 32; w++) v += red[w * P + k];
+      for (int w = 0; w < kGW; w++) v += red[w * P + k];
       a.grads[(size_t)li * P + k] = v;
     }
     __syncthreads();
@@ -356,8 +384,8 @@ __global__ void k_grad_sum(const double *grads, int64_t k_local, int P, double *
 
 size_t grad_smem_bytes(int max_N, int d) {
   const int ds = d <= 16 ? (d <= 4 ? 4 : d <= 8 ? 8 : d <= 10 ? 10 : d <= 12 ? 12 : 16) : d;
-  return sizeof(double) * ((size_t)max_N * ds + 3 * (size_t)max_N + 8 * (size_t)(d + 2) + SBV_MAX_D +
-                           8 * 32 * 33);
+  return sizeof(double) * ((size_t)max_N * ds + 4 * (size_t)max_N + kGW * (size_t)(d + 2) + SBV_MAX_D +
+                           kGW * 32 * 33);
 }
 
 static int grad_dm(int d) {

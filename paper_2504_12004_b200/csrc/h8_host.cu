@@ -12,7 +12,8 @@ static int h8_np_max(int max_N) { return (max_N + kPanel - 1) / kPanel; }
 static int h8_max_tasks(int max_N) {
   const int np = h8_np_max(max_N), nch0 = (((np * kPanel + 8) >> 3) + 3) >> 2;
   int n = 0;
-  for (int j = 0; j < np; j++) n += 2 * (nch0 - j) + 1;
+  // per panel: A x nch, BC x (nch - 1), F, C0, A2 (SBV_A0_EARLY)
+  for (int j = 0; j < np; j++) n += 2 * (nch0 - j) + 2;
   return n + 4;
 }
 
@@ -126,6 +127,7 @@ cudaError_t launch_h8_problem(const H8Problem &pb, int d, const double *theta, u
   a.tau2 = theta[d + 2];
   a.nu = theta[d + 1];
   for (int j = 0; j < SBV_MAX_D; j++) a.inv_beta[j] = j < d ? 1.0 / theta[1 + j] : 0.0;
+  a.theta_d = pb.theta_d;
   a.ws = pb.ws;
   a.ws_per_cta = pb.ws_per_cta;
   a.vs_off = h8_l_doubles(pb.max_N);
@@ -204,7 +206,7 @@ cudaError_t launch_h8_problem(const H8Problem &pb, int d, const double *theta, u
   return cudaGetLastError();
 }
 
-cudaError_t launch_h8(const Ctx &c, const double *theta, cudaStream_t st) {
+cudaError_t launch_h8(const Ctx &c, const double *theta, cudaStream_t st, const double *theta_dev) {
   H8Problem pb{};
   pb.Xp = c.Xperm;
   pb.yperm = c.yperm;
@@ -227,6 +229,7 @@ cudaError_t launch_h8(const Ctx &c, const double *theta, cudaStream_t st) {
   pb.n_big = c.h8_n_big;
   pb.max_N_small = c.h8_max_N_small;
   pb.grid_small = c.h8_grid_small;
+  pb.theta_d = theta_dev;
   return launch_h8_problem(pb, c.d, theta, c.queue, st);
 }
 

@@ -136,6 +136,9 @@ void free_state(sbv_ctx *h) {
   release(h->zws);
   release(h->grads);
   release(h->gsum);
+  release(h->theta_dev);
+  if (h->g_exec) cudaGraphExecDestroy(h->g_exec);
+  h->g_exec = nullptr;
   h->cap.clear();
   h->prepared = false;
 }
@@ -303,6 +306,59 @@ int validate_theta(sbv_ctx *h, const double *theta) {
   return SBV_OK;
 }
 
+// sbv_loglik replayed from a CUDA graph (sbv_set_graph; one GPU, device y):
+// H7 -> H8 -> H9 -> D2H of the result, captured on a private stream once per
+// (y pointer, nu, prepare) and launched on the handle's stream; theta reaches
+// the kernels through a pinned host -> device copy node (H8Args::theta_d), so
+// a new theta needs no re-capture.  Same kernels, same results bit for bit.
+int run_loglik_graph(sbv_ctx *h, const double *y, const double *theta) {
+  const int d = h->d;
+  const double nu = theta[d + 1];
+  if (!h->g_exec || h->g_y != y || h->g_nu != nu || h->g_gen != h->prep_gen) {
+    if (h->g_exec) {
+      cudaGraphExecDestroy(h->g_exec);
+      h->g_exec = nullptr;
+    }
+    if (!h->g_stream) CU(cudaStreamCreateWithFlags(&h->g_stream, cudaStreamNonBlocking));
+    if (!h->theta_pin) CU(cudaMallocHost(&h->theta_pin, (SBV_MAX_D + 3) * sizeof(double)));
+    CU(ensure(h->theta_dev, SBV_MAX_D + 3, h->cap));
+    cudaGraph_t g = nullptr;
+    CU(cudaStreamBeginCapture(h->g_stream, cudaStreamCaptureModeRelaxed));
+    cudaError_t e = cudaMemcpyAsync(h->theta_dev, h->theta_pin, (d + 3) * sizeof(double),
+                                    cudaMemcpyHostToDevice, h->g_stream);
+    if (!e) e = launch_stage_eval(y, h->perm, h->n, h->yperm, h->g_stream);
+    if (!e) e = launch_h8(*h, theta, h->g_stream, h->theta_dev);
+    if (!e) e = launch_reduce_chunks(*h, h->g_stream);
+    if (!e) e = launch_final_reduce(*h, h->g_stream);
+    if (!e) e = cudaMemcpyAsync(h->result_host, h->result, 8 * sizeof(double), cudaMemcpyDeviceToHost,
+                                h->g_stream);
+    const cudaError_t e2 = cudaStreamEndCapture(h->g_stream, &g);
+    if (!e) e = e2;
+    if (!e) e = cudaGraphInstantiate(&h->g_exec, g, 0);
+    if (g) cudaGraphDestroy(g);
+    if (e) {
+      h->g_exec = nullptr;
+      cudaGetLastError();
+      return fail(h, SBV_ERR_CUDA, cudaGetErrorString(e));
+    }
+    h->g_y = y;
+    h->g_nu = nu;
+    h->g_gen = h->prep_gen;
+  }
+  memcpy(h->theta_pin, theta, (d + 3) * sizeof(double));  // the previous replay has completed
+  CU(cudaGraphLaunch(h->g_exec, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  if (h->result_host[4] > 0) {
+    h->err_block = (int64_t)h->result_host[5];
+    h->err_stage = (int32_t)h->result_host[6];
+    h->err_msg = "Cholesky factorisation failed (non-positive pivot)";
+    return SBV_ERR_NOT_PD;
+  }
+  h->err_block = -1;
+  h->err_stage = 0;
+  return SBV_OK;
+}
+
 // Steps 4-5 for the current handle; leaves per-block outputs on device and
 // the reduced vector in h->result_host.
 // partials != nullptr: stop after H9 and copy this rank's chunk partials
@@ -316,6 +372,8 @@ int run_loglik(sbv_ctx *h, const double *y, const double *theta, double *partial
   int rc = validate_theta(h, theta);
   if (rc) return rc;
   CU(cudaSetDevice(h->device));
+  if (h->use_graph && !partials && h->world == 1 && !h->profile && is_device_ptr(y))
+    return run_loglik_graph(h, y, theta);
   Timer tm(h, 0);
   const double *yd = y;
   if (!is_device_ptr(y)) {
@@ -449,6 +507,8 @@ void sbv_destroy(sbv_handle h) {
   if (h->result_host) cudaFreeHost(h->result_host);
   if (h->flag_host) cudaFreeHost(h->flag_host);
   if (h->pin) cudaFreeHost(h->pin);
+  if (h->theta_pin) cudaFreeHost(h->theta_pin);
+  if (h->g_stream) cudaStreamDestroy(h->g_stream);
   delete h;
 }
 
@@ -756,6 +816,7 @@ int prepare_impl(sbv_ctx *h, const double *X, int64_t n, int32_t d, int32_t bs, 
   tm.mark("meta");
   tm.finish();
   h->prepared = true;
+  h->prep_gen++;
   return SBV_OK;
 }
 
@@ -817,6 +878,12 @@ int sbv_set_shard(sbv_handle h, int32_t rank, int32_t world) {
   }
   h->rank = rank;
   h->world = world;
+  return SBV_OK;
+}
+
+int sbv_set_graph(sbv_handle h, int32_t enable) {
+  if (!h || enable < 0 || enable > 1) return SBV_ERR_ARG;
+  h->use_graph = enable;
   return SBV_OK;
 }
 
@@ -922,7 +989,8 @@ int sbv_loglik_grad(sbv_handle h, const double *y, const double *theta, double *
   CU(cudaMemcpyAsync(h->lg_off, lgo.data(), h->k_local * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   int max_b = 1;
   for (int64_t li = 0; li < h->k_local; li++) max_b = std::max(max_b, h->Nt[li] - std::min<int32_t>(h->m, h->Nt[li]));
-  const int bpad_max = (h->max_bs + 31) & ~31;
+  // Z row stride: round4(b) contraction columns + the at column, in 32-column units
+  const int bpad_max = ((((h->max_bs + 3) & ~3) + 1) + 31) & ~31;
   int sms = 0;
   CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
   const int ggrid = (int)std::min<int64_t>(sms, std::max<int64_t>(h->k_local, 1));

@@ -102,6 +102,17 @@ struct Ctx {
   double *zws = nullptr;          // gradient: per-CTA Z scratch
   double *grads = nullptr;        // gradient: [k_local][d+2]
   double *gsum = nullptr;         // gradient: [d+2]
+  // CUDA-graph replay of sbv_loglik (sbv_set_graph): captured once per
+  // (y pointer, nu, prepare), theta through a pinned host -> device copy node
+  int use_graph = 0;
+  int64_t prep_gen = 0;           // bumped by every prepare (invalidates the graph)
+  cudaStream_t g_stream = nullptr;
+  cudaGraphExec_t g_exec = nullptr;
+  const double *g_y = nullptr;
+  double g_nu = 0.0;
+  int64_t g_gen = -1;
+  double *theta_pin = nullptr;    // pinned SBV_MAX_D + 3
+  double *theta_dev = nullptr;    // device SBV_MAX_D + 3
   size_t ws_per_cta = 0;
   int h8_grid = 0;
   int64_t h8_n_big = 0;           // split H8 launch (h8_split_plan)
@@ -181,7 +192,8 @@ void h8_split_plan(const int32_t *Nt_order, int64_t k, int d, int sms, int64_t *
                    int *grid_small);
 size_t h8_ws_doubles(int max_N, int d);
 int h8_max_ctas_per_sm(size_t smem, int d);
-cudaError_t launch_h8(const Ctx &c, const double *theta_host, cudaStream_t st);
+cudaError_t launch_h8(const Ctx &c, const double *theta_host, cudaStream_t st,
+                      const double *theta_dev = nullptr);
 // One H8 launch over an explicit set of blocks (estimation or prediction mode)
 struct H8Problem {
   const double *Xp, *yperm;        // training inputs / observations, block-major
@@ -198,6 +210,7 @@ struct H8Problem {
   int predict;                     // 1: B rows are test points Xq, outputs pmean / pvar; 2: keep L (gradient)
   int64_t n_big = 0;               // split launch: the first n_big work items (N > 2-CTA cap) alone
   int max_N_small = 0, grid_small = 0;
+  const double *theta_d = nullptr; // graph replay: theta in device memory (H8Args::theta_d)
   double *Lg = nullptr;            // predict == 2: per-block factor copies
   const int64_t *lg_off = nullptr;
   const double *Xq;

@@ -46,7 +46,7 @@ EXPORTS = ["sbv_abi_version", "sbv_create", "sbv_destroy", "sbv_comm_unique_id",
            "sbv_get_neighbors", "sbv_stats", "sbv_stage_times", "sbv_last_error",
            "sbv_predict", "sbv_get_prediction", "sbv_simulate", "sbv_set_shard",
            "sbv_partials_size", "sbv_loglik_partials", "sbv_reduce_partials",
-           "sbv_loglik_grad"]
+           "sbv_loglik_grad", "sbv_set_graph"]
 
 
 def lib():
@@ -68,6 +68,7 @@ def lib():
                                      ctypes.POINTER(_p)]
         L.sbv_prepare.argtypes = [_p, _i64, _i32, _i32, _i32, _p, ctypes.POINTER(_p)]
         L.sbv_set_shard.argtypes = [_p, _i32, _i32]
+        L.sbv_set_graph.argtypes = [_p, _i32]
         L.sbv_loglik_grad.argtypes = [_p, _p, _p, ctypes.POINTER(ctypes.c_double), _p]
         L.sbv_partials_size.argtypes = [_p, ctypes.POINTER(_i64)]
         L.sbv_loglik_partials.argtypes = [_p, _p, _p, _p]
@@ -162,6 +163,10 @@ class Handle:
     def comm_init(self, unique_id: bytes, rank: int, world: int):
         buf = ctypes.create_string_buffer(unique_id, 128)
         self._check(lib().sbv_comm_init(self._h, buf, rank, world))
+
+    def set_graph(self, enable: bool = True):
+        """sbv_set_graph: replay loglik from a CUDA graph (device y, one GPU)."""
+        self._check(lib().sbv_set_graph(self._h, 1 if enable else 0))
 
     def set_shard(self, rank: int, world: int):
         """sbv_set_shard: shard without a communicator (caller-side exchange)."""

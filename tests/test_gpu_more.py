@@ -282,3 +282,36 @@ def test_cfg4_shape_sampled(sbv, orc):
         assert abs(terms[t] - to) <= TOL_TERM * b, (t, terms[t], to)
     report("cfg4_shape_5M_sampled", blocks=[int(t) for t in ts], max_N=int(Nt.max()),
            max_rel_term_q18b=worst)
+
+
+def test_graph_replay_bit_identical(sbv, orc):
+    """sbv_set_graph (the cfg1 latency path): the captured H7 -> H8 -> H9 graph
+    gives the stream path's ell bit for bit, for a new theta without
+    re-capture, a new y buffer, a different nu and after a re-prepare; the
+    oracle pins the first value (north-star 1e-9)."""
+    import torch
+    n, d, bs, m = 20_000, 10, 20, 60  # cfg1 shape
+    X = si.make_X(n, d, seed=61)
+    y = si.make_y(X, seed=62)
+    scale = si.default_scale(d)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    thetas = [si.default_theta(d, nu=2.5, tau2=1e-4), si.default_theta(d, nu=2.5, tau2=3e-3)]
+    thetas[1][0] = 1.7
+    thetas[1][3] *= 1.3
+    th_nu = si.default_theta(d, nu=1.5, tau2=1e-4)
+    ref = sbv.Handle(seed=3)
+    ref.prepare(Xd, bs, m, scale)
+    want = [ref.loglik(yd, t) for t in thetas + [th_nu]]
+    h = sbv.Handle(seed=3)
+    h.set_graph(True)
+    h.prepare(Xd, bs, m, scale)
+    got = [h.loglik(yd, thetas[0]), h.loglik(yd, thetas[1]), h.loglik(yd, thetas[0]), h.loglik(yd, th_nu)]
+    assert got == [want[0], want[1], want[0], want[2]]
+    y2 = yd.clone()
+    assert h.loglik(y2, thetas[1]) == want[1]
+    h.prepare(Xd, bs, m, scale)
+    assert h.loglik(y2, thetas[0]) == want[0]
+    P = orc.prepare(X, bs, m, scale, 3)
+    ll_o = orc.loglik(X, y, P["perm"], P["off"], P["nbr"], P["cnt"], thetas[0])
+    report("graph_replay_cfg1", rel_ll=abs(want[0] - ll_o) / abs(ll_o))
+    assert abs(want[0] - ll_o) <= TOL_LL * abs(ll_o)

@@ -1,85 +1,64 @@
-"""Summarise gpurun_out/ ncu artefacts into profiles/<round>/ (tracked).
-
-    python tools/summarize_profiles.py r01
-"""
-import csv
-import io
-import json
-import os
-import subprocess
-import sys
+"""Summarise one profiling pass (tools/gpu_r2_prof.sh outputs in gpurun_out/) into profiles/<round>/:
+    python tools/summarize_profiles.py TAG ROUND_DIR
+-> <ROUND_DIR>/h8_full_ncu_summary.json, knn_full_ncu_summary.json (selected metrics of the
+   `ncu --set full` raw page) and launch_list_summary.json (per-kernel share of the launch list)."""
+import csv, io, json, os, sys
 from collections import defaultdict
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-OUT = os.path.join(ROOT, "gpurun_out")
+tag, out = sys.argv[1], sys.argv[2]
+src = "gpurun_out"
+KEEP = ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "l1tex__t_sector_hit_rate.pct",
+        "launch__block_size", "launch__grid_size", "launch__registers_per_thread",
+        "lts__t_sector_hit_rate.pct", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+        "sm__instruction_throughput.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "Kernel Name")
 
 
-def launches(tag):
-    path = os.path.join(OUT, "launches.csv")
-    rows = []
-    with open(path) as f:
-        lines = [ln for ln in f if ln.startswith('"')]
-    rd = csv.reader(io.StringIO("".join(lines)))
-    hdr = next(rd)
-    iK, iM, iV = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
-    iU = hdr.index("Metric Unit")
-    for r in rd:
-        if r[iM] != "gpu__time_duration.sum":
-            continue
-        v = float(r[iV].replace(",", ""))
-        unit = r[iU]
-        ns = v * {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9}.get(unit, 1)
-        rows.append((r[iK].split("(")[0].replace("void ", ""), ns))
-    agg = defaultdict(lambda: [0, 0.0])
-    for k, ns in rows:
-        agg[k][0] += 1
-        agg[k][1] += ns
-    tot = sum(v[1] for v in agg.values())
-    summary = sorted(({"kernel": k, "launches": c, "total_ms": t / 1e6, "share": t / tot}
-                      for k, (c, t) in agg.items()), key=lambda x: -x["total_ms"])
-    return {"command": "python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-predict",
-            "note": "ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised); "
-                    "compare SHARES, not absolute times",
-            "total_launches": len(rows), "kernels": summary}
-
-
-def raw_metrics(rep):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    r = list(csv.reader(io.StringIO(raw)))
-    hdr, units, vals = r[0], r[1], r[2]
-    want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-            "lts__t_bytes.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
-            "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
-            "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
-            "smsp__issue_active.avg.pct_of_peak_sustained_active",
-            "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
-            "launch__grid_size", "launch__block_size", "smsp__inst_executed.sum",
-            "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct"]
-    out = {}
+def raw_summary(path):
+    rows = list(csv.reader(open(path)))
+    i = next(k for k, r in enumerate(rows) if r and r[0] == "ID")
+    hdr, units, vals = rows[i], rows[i + 1], rows[i + 2]
+    d = {}
     for h, u, v in zip(hdr, units, vals):
-        if h in want or (h.startswith("smsp__average_warps_issue_stalled") and h.endswith("per_issue_active.ratio")):
+        if h in KEEP or (h.startswith("smsp__average_warps_issue_stalled") and h.endswith("per_issue_active.ratio")):
             try:
-                fv = float(v.replace(",", ""))
-                if h.startswith("smsp__average_warps_issue_stalled") and fv < 0.2:
-                    continue
-                out[h] = [fv, u]
+                d[h] = [float(v.replace(",", "")), u]
             except ValueError:
-                out[h] = [v, u]
-    return out
+                d[h] = [v, u]
+    d["source"] = f"ncu --set full --clock-control none, {os.path.basename(path)} (tools/gpu_r2_prof.sh, TAG={tag})"
+    return d
 
 
-def main():
-    tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
-    dst = os.path.join(ROOT, "profiles", tag)
-    os.makedirs(dst, exist_ok=True)
-    if os.path.exists(os.path.join(OUT, "launches.csv")):
-        json.dump(launches(tag), open(os.path.join(dst, "launch_list_summary.json"), "w"), indent=1)
-    for name in ["h8_full", "knn_full"]:
-        rep = os.path.join(OUT, name + ".ncu-rep")
-        if os.path.exists(rep):
-            json.dump(raw_metrics(rep), open(os.path.join(dst, name + "_ncu_summary.json"), "w"), indent=1)
-    print("wrote", os.listdir(dst))
+os.makedirs(out, exist_ok=True)
+for name, fn in (("h8", "h8_full_ncu_summary.json"), ("knn", "knn_full_ncu_summary.json")):
+    p = os.path.join(src, f"{tag}_{name}_raw.csv")
+    if os.path.exists(p):
+        json.dump(raw_summary(p), open(os.path.join(out, fn), "w"), indent=1)
+        print("wrote", fn)
 
-
-if __name__ == "__main__":
-    main()
+p = os.path.join(src, f"{tag}_launches.csv")
+if os.path.exists(p):
+    lines = [l for l in open(p) if l.startswith('"')]
+    rows = list(csv.DictReader(io.StringIO("".join(lines))))
+    tot, cnt = defaultdict(float), defaultdict(int)
+    for r in rows:
+        if r["Metric Name"] != "gpu__time_duration.sum":
+            continue
+        v = float(r["Metric Value"].replace(",", ""))
+        scale = {"ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "nsecond": 1e-6}.get(r["Metric Unit"], 1.0)
+        k = r["Kernel Name"].split("(")[0]
+        tot[k] += v * scale
+        cnt[k] += 1
+    s = sum(tot.values())
+    ks = sorted(tot, key=lambda k: -tot[k])
+    json.dump({"command": "python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-predict",
+               "note": "ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised); compare SHARES, not absolute times",
+               "tag": tag, "total_launches": sum(cnt.values()),
+               "kernels": [{"kernel": k, "launches": cnt[k], "total_ms": tot[k], "share": tot[k] / s} for k in ks]},
+              open(os.path.join(out, "launch_list_summary.json"), "w"), indent=1)
+    print("wrote launch_list_summary.json", [(k, round(tot[k] / s, 3)) for k in ks[:4]])
