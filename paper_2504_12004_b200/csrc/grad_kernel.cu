@@ -34,7 +34,10 @@
 
 namespace sbv {
 
-constexpr int kGThreads = 256;
+#ifndef SBV_GRAD_WARPS
+#define SBV_GRAD_WARPS 4  // warps per CTA (4: two CTAs per SM at <= 255 registers)
+#endif
+constexpr int kGThreads = SBV_GRAD_WARPS * 32;
 
 struct GradArgs {
   const double *Lg;          // per-block (N+1) x N row-major factor copies
@@ -115,7 +118,7 @@ __device__ __forceinline__ void gemm_pf(double (&acc)[4][NCT][2], int kb, int ke
 // DM > 0: coordinates staged with the padded row stride DM (d <= DM, zero
 // padded; the padded dimensions contribute 0 to every distance and gradient)
 template <int NU2, int DM>
-__global__ void __launch_bounds__(kGThreads, 1) k_grad(GradArgs a) {
+__global__ void __launch_bounds__(kGThreads, 8 / SBV_GRAD_WARPS) k_grad(GradArgs a) {
   extern __shared__ double gsm[];
   __shared__ int s_item;
   __shared__ double s_etab[256];
@@ -172,8 +175,9 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grad(GradArgs a) {
       for (int p = NPn - 1; p >= 0; p--) {
         const int r0 = p * 32;
         double acc[4][NCT][2];
-        // right-hand sides at the panel rows: 1 at (mt + c, c) for c < bb,
-        // y'_J in column cz4
+        // acc holds the NEGATED partial solution (no operand negation in the
+        // k-loop): -(right-hand sides) at the panel rows, i.e. -1 at
+        // (mt + c, c) for c < bb and -y'_J in column cz4
 #pragma unroll
         for (int rt = 0; rt < 4; rt++)
 #pragma unroll
@@ -181,15 +185,15 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grad(GradArgs a) {
 #pragma unroll
             for (int i = 0; i < 2; i++) {
               const int row = r0 + rt * 8 + g, col = cb + ct * 8 + 2 * q + i;
-              acc[rt][ct][i] = col < bb ? (row == mt + col ? 1.0 : 0.0) : (col == cz4 && row < mt ? yp[row] : 0.0);
+              acc[rt][ct][i] = col < bb ? (row == mt + col ? -1.0 : 0.0) : (col == cz4 && row < mt ? -yp[row] : 0.0);
             }
-        // acc -= L[k, panel cols]^T Z[k, slice cols] over rows k >= r0 + 32
+        // acc += L[k, panel cols]^T Z[k, slice cols] over rows k >= r0 + 32
         gemm_pf<NCT>(
             acc, r0 + 32, N,
             [&](int k0, double (&A)[4]) {
               const int kr = k0 + q;
 #pragma unroll
-              for (int rt = 0; rt < 4; rt++) A[rt] = (kr < N) ? -L[(size_t)kr * N + r0 + rt * 8 + g] : 0.0;
+              for (int rt = 0; rt < 4; rt++) A[rt] = (kr < N) ? L[(size_t)kr * N + r0 + rt * 8 + g] : 0.0;
             },
             [&](int k0, double (&B)[NCT]) {
               const int kr = k0 + q;
@@ -204,7 +208,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grad(GradArgs a) {
 #pragma unroll
             for (int i = 0; i < 2; i++) {
               const int row = r0 + rt * 8 + g, col = cb + ct * 8 + 2 * q + i;
-              if (row < N) Z[(size_t)row * bpad + col] = acc[rt][ct][i];
+              if (row < N) Z[(size_t)row * bpad + col] = -acc[rt][ct][i];
             }
         const int nr = min(32, N - r0);
 #pragma unroll 8
@@ -409,6 +413,24 @@ static void (*pick_grad(int dm))(GradArgs) {
   }
 }
 
+static void (*pick_grad_fn(double nu, int d))(GradArgs) {
+  const int dm = grad_dm(d);
+  return nu == 0.5 ? pick_grad<1>(dm) : nu == 1.5 ? pick_grad<3>(dm) : nu == 2.5 ? pick_grad<5>(dm) : pick_grad<7>(dm);
+}
+
+// persistent grid: resident CTAs per SM (shared memory / registers) x SMs
+int grad_grid(double nu, int d, int max_N, int sms) {
+  void (*f)(GradArgs) = pick_grad_fn(nu, d);
+  const size_t sm = grad_smem_bytes(max_N, d);
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kGThreads, sm) != cudaSuccess || nb < 1) {
+    cudaGetLastError();
+    nb = 1;
+  }
+  return sms * nb;
+}
+
 cudaError_t launch_grad(const GradLaunch &gl, cudaStream_t st) {
   GradArgs a;
   a.Lg = gl.Lg;
@@ -434,8 +456,7 @@ cudaError_t launch_grad(const GradLaunch &gl, cudaStream_t st) {
   if (e) return e;
   if (gl.n_items == 0) return cudaSuccess;
   const double nu = gl.theta[gl.d + 1];
-  const int dm = grad_dm(gl.d);
-  void (*f)(GradArgs) = nu == 0.5 ? pick_grad<1>(dm) : nu == 1.5 ? pick_grad<3>(dm) : nu == 2.5 ? pick_grad<5>(dm) : pick_grad<7>(dm);
+  void (*f)(GradArgs) = pick_grad_fn(nu, gl.d);
   const size_t sm = grad_smem_bytes(gl.max_N, gl.d);
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   f<<<gl.grid, kGThreads, sm, st>>>(a);

@@ -993,7 +993,8 @@ int sbv_loglik_grad(sbv_handle h, const double *y, const double *theta, double *
   const int bpad_max = ((((h->max_bs + 3) & ~3) + 1) + 31) & ~31;
   int sms = 0;
   CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-  const int ggrid = (int)std::min<int64_t>(sms, std::max<int64_t>(h->k_local, 1));
+  const int ggrid = (int)std::min<int64_t>(grad_grid(theta[d + 1], d, std::max(h->max_N, 1), sms),
+                                           std::max<int64_t>(h->k_local, 1));
   CU(ensure(h->zws, (int64_t)ggrid * std::max(h->max_N, 1) * std::max(bpad_max, 32), cap));
   CU(ensure(h->grads, std::max<int64_t>(h->k_local, 1) * P, cap));
   CU(ensure(h->gsum, P, cap));

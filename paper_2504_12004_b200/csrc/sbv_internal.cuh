@@ -233,6 +233,7 @@ struct GradLaunch {
   double *grads;
 };
 size_t grad_smem_bytes(int max_N, int d);
+int grad_grid(double nu, int d, int max_N, int sms);
 cudaError_t launch_grad(const GradLaunch &gl, cudaStream_t st);
 cudaError_t launch_grad_sum(const double *grads, int64_t k_local, int P, double *out, cudaStream_t st);
 cudaError_t launch_reduce_chunks(const Ctx &c, cudaStream_t st);

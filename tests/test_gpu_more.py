@@ -315,3 +315,29 @@ def test_graph_replay_bit_identical(sbv, orc):
     ll_o = orc.loglik(X, y, P["perm"], P["off"], P["nbr"], P["cnt"], thetas[0])
     report("graph_replay_cfg1", rel_ll=abs(want[0] - ll_o) / abs(ll_o))
     assert abs(want[0] - ll_o) <= TOL_LL * abs(ll_o)
+
+
+def test_prepare_from_freed_temporary_on_side_stream(sbv):
+    """sbv.h: X is read only during the call.  A handle on a non-blocking side
+    stream prepares from a temporary device tensor that is freed on return and
+    whose memory torch immediately reuses (overwritten with NaN on its own
+    stream): ell must equal the default-stream handle's bit for bit."""
+    import torch
+    n, d, bs, m = 50_000, 10, 50, 100
+    X = si.make_X(n, d, seed=71)
+    yd = torch.from_numpy(si.make_y(X, seed=72)).cuda()
+    scale = si.default_scale(d)
+    theta = si.default_theta(d, nu=2.5, tau2=1e-4)
+    ref = sbv.Handle(seed=3)
+    ref.prepare(torch.from_numpy(X).cuda(), bs, m, scale)
+    want = ref.loglik(yd, theta)
+    side = torch.cuda.Stream()
+    h = sbv.Handle(seed=3, stream=side)
+    for _ in range(3):
+        Xt = torch.from_numpy(X).cuda()
+        h.prepare(Xt, bs, m, scale)
+        del Xt
+        junk = torch.full((n, d), float("nan"), dtype=torch.float64, device="cuda")  # reuses the block
+        del junk
+    torch.cuda.synchronize()
+    assert h.loglik(yd, theta) == want

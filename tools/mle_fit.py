@@ -21,6 +21,7 @@ from scipy import optimize
 
 import sbv_inputs as si
 import paper_2504_12004_b200 as sbv
+from bench import Clocks
 
 
 def main():
@@ -77,6 +78,8 @@ def main():
     # re-prepare slow: the <= 3-dim grid prunes poorly when all 10 dims
     # matter)
     z0 = np.log(np.array([1.0, *(2.0 * np.array(si.PAPER_BETA_D10)), 1e-2]))
+    clocks = Clocks(torch.cuda.current_device())
+    clocks.start()
     t0 = time.perf_counter()
     if args.method == "lbfgs":
         res = optimize.minimize(nll_grad, z0, jac=True, method="L-BFGS-B",
@@ -85,12 +88,14 @@ def main():
         res = optimize.minimize(nll, z0, method="Nelder-Mead",
                                 options={"maxfev": args.evals, "xatol": 1e-3, "fatol": 1e-3})
     wall = time.perf_counter() - t0
+    ck = clocks.stop()
     print(json.dumps({"config": f"cfg3: n={args.n} d={d} bs={bs} m={m} nu={nu}, y smooth (2 relevant dims)",
                       "method": args.method,
                       "evals": len(hist), "wall_s": wall, "gpu_ms_per_eval_mean": float(np.mean(gpu_ms)),
                       "ll_start": hist[0], "ll_best": float(-res.fun),
                       "beta_best": np.exp(res.x[1:1 + d]).round(4).tolist(),
                       "sigma2_best": float(np.exp(res.x[0])), "tau2_best": float(np.exp(res.x[-1])),
+                      "clocks": ck,
                       "note": "each eval = sbv_prepare_h (rescale) + sbv_loglik (lbfgs: sbv_loglik_grad); optimiser on the host"}))
 
 
