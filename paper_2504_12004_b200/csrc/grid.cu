@@ -630,7 +630,10 @@ __device__ void warp_select(const WCand *buf, int cnt, int m, int lane, unsigned
 // warps split one query's candidates and meet at every ring end, for small
 // query counts where a single wave of one-warp queries is latency-bound).
 template <int DM, int QW>
-__global__ void __launch_bounds__(32 * kKnnWarps) k_knn_grid(
+#ifndef SBV_KNN_MINB
+#define SBV_KNN_MINB 1  // min resident CTAs per SM asked of ptxas (register cap)
+#endif
+__global__ void __launch_bounds__(32 * kKnnWarps, SBV_KNN_MINB) k_knn_grid(
     const double *__restrict__ Sperm, const int32_t *__restrict__ perm,
     const int64_t *__restrict__ off, const double *__restrict__ C,
     const int32_t *__restrict__ local_blocks, int64_t k_local, int d, int m, KnnLevels lv,

@@ -85,3 +85,36 @@ def test_grad_rejects_general_nu(sbv):
     with pytest.raises(sbv.SBVError) as e:
         h.loglik_grad(np.zeros(500), np.array([1.0, 1, 1, 1, 1.3, 1e-3]))
     assert e.value.code == 5
+
+
+def test_grad_cfg2_full_size_central_differences(sbv):
+    """BASELINE cfg2 at full size (n = 1M, d = 10, bs = 100, m = 200, nu = 2.5,
+    the bench's launch configuration) where the oracle's explicit inverses
+    are out of reach: every gradient component against a central difference
+    of sbv_loglik itself (parity-pinned to the oracle at 1e-9), step 1e-5
+    relative; the truncation error (h^2 l'''/6) and the rounding noise of the
+    deterministic ell are both below 1e-7 of the components here."""
+    import torch
+    c = si.CONFIGS["cfg2"]
+    n, d, bs, m = c["n"], c["d"], c["bs"], c["m"]
+    X = torch.from_numpy(si.make_X(n, d, seed=1)).cuda()
+    y = torch.randn(n, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(2))
+    theta = si.default_theta(d, nu=c["nu"], tau2=1e-4)
+    h = sbv.Handle(seed=3)
+    h.prepare(X, bs, m, si.default_scale(d))
+    ll, g = h.loglik_grad(y, theta)
+    assert ll == h.loglik(y, theta)
+    idx = [0, *range(1, d + 1), d + 2]  # sigma2, beta_1..beta_d, tau2 (nu fixed)
+    fd = np.zeros(len(idx))
+    for k, i in enumerate(idx):
+        step = 1e-5 * theta[i]
+        tp, tm = theta.copy(), theta.copy()
+        tp[i] += step
+        tm[i] -= step
+        fd[k] = (h.loglik(y, tp) - h.loglik(y, tm)) / (tp[i] - tm[i])
+    rel = np.abs(g - fd) / np.maximum(np.abs(g), np.abs(g).max() * 1e-6)
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "parity_report.jsonl"), "a") as f:
+        f.write(json.dumps({"test": "grad_cfg2_central_differences", "max_rel": float(rel.max()),
+                            "rel": rel.tolist()}) + "\n")
+    assert rel.max() <= 1e-6, (rel, g, fd)
