@@ -153,6 +153,13 @@ int sbv_loglik(sbv_handle h, const double *y, const double *theta, double *ll);
  * for nu outside {0.5, 1.5, 2.5, 3.5} or world > 1. */
 int sbv_loglik_grad(sbv_handle h, const double *y, const double *theta, double *ll, double *grad);
 
+/* The per-block gradients d ell_t / d (sigma2, beta_1..beta_d, tau2) of the
+ * last successful sbv_loglik_grad (whose sum in block order is its grad):
+ * host or device double[bc x (d+2)], row t = block t (zeta order).
+ * Errors: SBV_ERR_STATE (no successful sbv_loglik_grad since the last
+ * prepare), SBV_ERR_ARG, SBV_ERR_CUDA. */
+int sbv_block_grads(sbv_handle h, double *grads);
+
 /* CUDA-graph replay of sbv_loglik (the latency case, cfg1: P:752 names
  * per-call overhead as what limits small problems).  enable = 1: on one GPU
  * (world 1) with a DEVICE y and profiling off, sbv_loglik / sbv_loglik_parts

@@ -631,7 +631,7 @@ __device__ void warp_select(const WCand *buf, int cnt, int m, int lane, unsigned
 // query counts where a single wave of one-warp queries is latency-bound).
 template <int DM, int QW>
 #ifndef SBV_KNN_MINB
-#define SBV_KNN_MINB 1  // min resident CTAs per SM asked of ptxas (register cap)
+#define SBV_KNN_MINB 5  // min resident CTAs per SM asked of ptxas (register cap; measured at cfg2: 1 / 5 / 6 / 8 -> 0.65 / 0.56 / 0.60 / 0.66 ms)
 #endif
 __global__ void __launch_bounds__(32 * kKnnWarps, SBV_KNN_MINB) k_knn_grid(
     const double *__restrict__ Sperm, const int32_t *__restrict__ perm,

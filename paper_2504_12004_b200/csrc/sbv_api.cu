@@ -881,6 +881,17 @@ int sbv_set_shard(sbv_handle h, int32_t rank, int32_t world) {
   return SBV_OK;
 }
 
+int sbv_block_grads(sbv_handle h, double *grads) {
+  if (!h || !grads) return SBV_ERR_ARG;
+  if (!h->prepared || h->grad_gen != h->prep_gen)
+    return fail(h, SBV_ERR_STATE, "sbv_block_grads needs a successful sbv_loglik_grad after the last prepare");
+  CU(cudaSetDevice(h->device));
+  CU(cudaMemcpyAsync(grads, h->grads, (size_t)h->k_local * (h->d + 2) * sizeof(double), cudaMemcpyDefault,
+                     h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  return SBV_OK;
+}
+
 int sbv_set_graph(sbv_handle h, int32_t enable) {
   if (!h || enable < 0 || enable > 1) return SBV_ERR_ARG;
   h->use_graph = enable;
@@ -1070,6 +1081,7 @@ int sbv_loglik_grad(sbv_handle h, const double *y, const double *theta, double *
   CU(launch_reduce_chunks(*h, st));
   CU(launch_final_reduce(*h, st));
   CU(launch_grad_sum(h->grads, h->k_local, P, h->gsum, st));
+  h->grad_gen = -1;
   CU(cudaMemcpyAsync(h->result_host, h->result, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
   CU(cudaMemcpyAsync(grad, h->gsum, P * sizeof(double), cudaMemcpyDefault, st));
   tm.mark("H9_grad_sums_d2h");
@@ -1082,6 +1094,7 @@ int sbv_loglik_grad(sbv_handle h, const double *y, const double *theta, double *
     return fail(h, SBV_ERR_NOT_PD, "Cholesky factorisation failed (non-positive pivot)");
   }
   *ll = h->result_host[0];
+  h->grad_gen = h->prep_gen;
   return SBV_OK;
 }
 

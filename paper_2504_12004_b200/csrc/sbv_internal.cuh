@@ -104,6 +104,7 @@ struct Ctx {
   double *gsum = nullptr;         // gradient: [d+2]
   // CUDA-graph replay of sbv_loglik (sbv_set_graph): captured once per
   // (y pointer, nu, prepare), theta through a pinned host -> device copy node
+  int64_t grad_gen = -1;          // prep_gen of the last successful sbv_loglik_grad (sbv_block_grads)
   int use_graph = 0;
   int64_t prep_gen = 0;           // bumped by every prepare (invalidates the graph)
   cudaStream_t g_stream = nullptr;

@@ -46,7 +46,7 @@ EXPORTS = ["sbv_abi_version", "sbv_create", "sbv_destroy", "sbv_comm_unique_id",
            "sbv_get_neighbors", "sbv_stats", "sbv_stage_times", "sbv_last_error",
            "sbv_predict", "sbv_get_prediction", "sbv_simulate", "sbv_set_shard",
            "sbv_partials_size", "sbv_loglik_partials", "sbv_reduce_partials",
-           "sbv_loglik_grad", "sbv_set_graph"]
+           "sbv_loglik_grad", "sbv_set_graph", "sbv_block_grads"]
 
 
 def lib():
@@ -69,6 +69,7 @@ def lib():
         L.sbv_prepare.argtypes = [_p, _i64, _i32, _i32, _i32, _p, ctypes.POINTER(_p)]
         L.sbv_set_shard.argtypes = [_p, _i32, _i32]
         L.sbv_set_graph.argtypes = [_p, _i32]
+        L.sbv_block_grads.argtypes = [_p, _p]
         L.sbv_loglik_grad.argtypes = [_p, _p, _p, ctypes.POINTER(ctypes.c_double), _p]
         L.sbv_partials_size.argtypes = [_p, ctypes.POINTER(_i64)]
         L.sbv_loglik_partials.argtypes = [_p, _p, _p, _p]
@@ -250,6 +251,12 @@ class Handle:
         self._check(lib().sbv_loglik_grad(self._h, py, th.ctypes.data_as(_p), ctypes.byref(out),
                                           g.ctypes.data_as(_p)))
         return out.value, g
+
+    def block_grads(self):
+        """sbv_block_grads: per-block gradients of the last loglik_grad, (bc, d+2)."""
+        out = np.zeros((self.num_blocks(), self.d + 2))
+        self._check(lib().sbv_block_grads(self._h, out.ctypes.data_as(_p)))
+        return out
 
     def loglik_parts(self, y, theta):
         y = _f64(y)
