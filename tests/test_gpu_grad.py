@@ -93,16 +93,17 @@ def test_grad_cfg2_full_size_central_differences(sbv):
     """BASELINE cfg2 at full size (n = 1M, d = 10, bs = 100, m = 200, nu = 2.5,
     the bench's launch configuration) where the oracle's explicit inverses
     are out of reach: every gradient component against a central difference
-    of sbv_loglik itself (parity-pinned to the oracle at 1e-9), steps 1e-5 and
-    2e-5 relative with Richardson extrapolation (truncation O(h^4), leaving
+    of sbv_loglik itself (parity-pinned to the oracle at 1e-9), steps 1e-4 and
+    2e-4 relative with Richardson extrapolation (truncation O(h^4), leaving
     the rounding noise of the deterministic ell).  Same bar as the oracle tests
     (Q28b: 1e-7 of max(|g_k|, sum_t |g_t,k|), the per-block gradients from
     sbv_block_grads)."""
     import torch
     c = si.CONFIGS["cfg2"]
     n, d, bs, m = c["n"], c["d"], c["bs"], c["m"]
-    X = torch.from_numpy(si.make_X(n, d, seed=1)).cuda()
-    y = torch.randn(n, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(2))
+    Xh = si.make_X(n, d, seed=1)
+    X = torch.from_numpy(Xh).cuda()
+    y = torch.from_numpy(si.make_y(Xh, seed=2)).cuda()  # smooth field + noise (the input recipe)
     theta = si.default_theta(d, nu=c["nu"], tau2=1e-4)
     h = sbv.Handle(seed=3)
     h.prepare(X, bs, m, si.default_scale(d))
@@ -118,7 +119,7 @@ def test_grad_cfg2_full_size_central_differences(sbv):
         return (h.loglik(y, tp) - h.loglik(y, tm)) / (tp[i] - tm[i])
 
     for k, i in enumerate(idx):  # Richardson: (4 D(h) - D(2h)) / 3 cancels the h^2 term
-        fd[k] = (4.0 * central(i, 1e-5) - central(i, 2e-5)) / 3.0
+        fd[k] = (4.0 * central(i, 1e-4) - central(i, 2e-4)) / 3.0
     gb = h.block_grads()  # per-block gradients: the Q28b base max(|g|, sum_t |g_t|)
     assert gb.shape == (h.num_blocks(), d + 2)
     base = np.maximum(np.abs(g), np.abs(gb).sum(0))
@@ -127,5 +128,5 @@ def test_grad_cfg2_full_size_central_differences(sbv):
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "parity_report.jsonl"), "a") as f:
         f.write(json.dumps({"test": "grad_cfg2_central_differences", "max_rel": float(rel.max()),
-                            "rel": rel.tolist()}) + "\n")
+                            "rel": rel.tolist(), "rel_to_abs_g": (np.abs(g - fd) / np.abs(g)).tolist()}) + "\n")
     assert rel.max() <= TOL_G, (rel, g, fd)
