@@ -93,9 +93,10 @@ def test_grad_cfg2_full_size_central_differences(sbv):
     """BASELINE cfg2 at full size (n = 1M, d = 10, bs = 100, m = 200, nu = 2.5,
     the bench's launch configuration) where the oracle's explicit inverses
     are out of reach: every gradient component against a central difference
-    of sbv_loglik itself (parity-pinned to the oracle at 1e-9), steps 1e-4 and
-    2e-4 relative with Richardson extrapolation (truncation O(h^4), leaving
-    the rounding noise of the deterministic ell).  Same bar as the oracle tests
+    of sbv_loglik itself (parity-pinned to the oracle at 1e-9), steps 1e-3 and
+    2e-3 relative with Richardson extrapolation (truncation O(h^4), leaving
+    the rounding noise of the deterministic ell, which falls as 1/h:
+    profiles/r02/grad_fd_check_cfg2.jsonl, 1e-6 ... 1e-3).  Same bar as the oracle tests
     (Q28b: 1e-7 of max(|g_k|, sum_t |g_t,k|), the per-block gradients from
     sbv_block_grads)."""
     import torch
@@ -119,7 +120,7 @@ def test_grad_cfg2_full_size_central_differences(sbv):
         return (h.loglik(y, tp) - h.loglik(y, tm)) / (tp[i] - tm[i])
 
     for k, i in enumerate(idx):  # Richardson: (4 D(h) - D(2h)) / 3 cancels the h^2 term
-        fd[k] = (4.0 * central(i, 1e-4) - central(i, 2e-4)) / 3.0
+        fd[k] = (4.0 * central(i, 1e-3) - central(i, 2e-3)) / 3.0
     gb = h.block_grads()  # per-block gradients: the Q28b base max(|g|, sum_t |g_t|)
     assert gb.shape == (h.num_blocks(), d + 2)
     base = np.maximum(np.abs(g), np.abs(gb).sum(0))
