@@ -395,7 +395,7 @@ __global__ void k_gather_anchor_rows(const double *__restrict__ S, const int32_t
 // Points are visited in anchor-grid cell order (`order`, relative to i0), so
 // the lanes of a warp search the same cells and read the same anchor rows.
 #ifndef SBV_RAC_MINB
-#define SBV_RAC_MINB 1  // CTAs per SM the RAC kernel's registers are bounded for
+#define SBV_RAC_MINB 4  // CTAs per SM the RAC kernel's registers are bounded for (measured at cfg2: 1 / 3 / 4 -> 0.43 / 0.37 / 0.35 ms)
 #endif
 template <int DM>
 __global__ void __launch_bounds__(256, SBV_RAC_MINB) k_rac_grid2(const double *__restrict__ S, const int32_t *__restrict__ order,

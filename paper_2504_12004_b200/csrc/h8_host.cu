@@ -89,6 +89,41 @@ size_t h8_ws_doubles(int max_N, int d) {
   return h8_l_doubles(max_N) + vs;
 }
 
+static H8Fn pick_small(double nu, int d) {
+  const int dm = h8_dm(d);
+  if (nu == 0.5) return h8_pick_small_nu1(dm);
+  if (nu == 1.5) return h8_pick_small_nu3(dm);
+  if (nu == 2.5) return h8_pick_small_nu5(dm);
+  return h8_pick_small_nu7(dm);
+}
+
+// A launch whose blocks are all small (max N <= kSmallMaxN: at most 6 panels,
+// where the per-block panel chain, not the bulk work, sets the block's time)
+// runs the SBV_H8_SMALL_WARPS-warp instantiation (4: 4 CTAs per SM, twice
+// the concurrent chains).  Log-likelihood mode with a closed-form nu only; SBV_H8_SMALL=0
+// disables it (A/B runs).
+constexpr int kSmallMaxN = 192;
+bool h8_use_small(int max_N) {
+  static const int env = [] {
+    const char *e = getenv("SBV_H8_SMALL");
+    return e ? atoi(e) : 1;
+  }();
+  return env != 0 && max_N <= kSmallMaxN;
+}
+static bool closed_form(double nu) { return nu == 0.5 || nu == 1.5 || nu == 2.5 || nu == 3.5; }
+
+int h8_small_ctas_per_sm(size_t smem, int d) {
+  int best = 1 << 30;
+  for (double nu : {0.5, 1.5, 2.5, 3.5}) {
+    const H8Fn f = pick_small(nu, d);
+    int nb = 0;
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, 32 * SBV_H8_SMALL_WARPS, smem);
+    best = nb < best ? nb : best;
+  }
+  return best;
+}
+
 static H8Fn pick(double nu, int d, int pred = 0) {
   const int dm = h8_dm(d);
   if (nu == 0.5) return h8_pick_nu1(dm, pred);
@@ -165,7 +200,11 @@ cudaError_t launch_h8_problem(const H8Problem &pb, int d, const double *theta, u
   a.trace_n = tn;
   a.trace_cap = cap;
 #endif
-  {
+  if (pb.small && pb.predict == 0 && closed_form(nu)) {
+    const H8Fn f = pick_small(nu, d);
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pb.smem);
+    f<<<pb.grid, 32 * SBV_H8_SMALL_WARPS, pb.smem, st>>>(a);
+  } else {
     const H8Fn f = pick(nu, d, pb.predict);
     if (pb.n_big > 0 && pb.n_big < pb.k_local) {
       // split launch (h8_two_cta_cap): the n_big largest blocks (first in the
@@ -229,6 +268,7 @@ cudaError_t launch_h8(const Ctx &c, const double *theta, cudaStream_t st, const 
   pb.n_big = c.h8_n_big;
   pb.max_N_small = c.h8_max_N_small;
   pb.grid_small = c.h8_grid_small;
+  pb.small = c.h8_small;
   pb.theta_d = theta_dev;
   return launch_h8_problem(pb, c.d, theta, c.queue, st);
 }

@@ -800,8 +800,11 @@ int prepare_impl(sbv_ctx *h, const double *X, int64_t n, int32_t d, int32_t bs, 
     h->occ_smem = h->h8_smem;
     h->occ_d = d;
     h->occ_per_sm = h8_max_ctas_per_sm(h->h8_smem, d);
+    h->occ_small = h8_small_ctas_per_sm(h->h8_smem, d);
   }
   int per_sm = h->occ_per_sm;
+  h->h8_small = h8_use_small(h->max_N) ? 1 : 0;
+  if (h->h8_small) per_sm = std::max(per_sm, h->occ_small);
   if (per_sm < 1) per_sm = 1;
   h->h8_grid = (int)std::min<int64_t>((int64_t)sms * per_sm, std::max<int64_t>(h->k_local, 1));
   {

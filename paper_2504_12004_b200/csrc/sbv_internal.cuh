@@ -118,9 +118,11 @@ struct Ctx {
   int h8_grid = 0;
   int64_t h8_n_big = 0;           // split H8 launch (h8_split_plan)
   int h8_max_N_small = 0, h8_grid_small = 0;
+  int h8_small = 0;               // 1: loglik launches use the 4-warp kernel (h8_use_small)
   size_t h8_smem = 0;
   size_t occ_smem = 0;  // cached occupancy query
   int occ_per_sm = 0;
+  int occ_small = 0;    // cached occupancy of the 4-warp kernel
   int occ_d = 0;
   KnnLevels lv{};                 // kNN prefix-level grids of the training set (prepare)
   bool lv_valid = false;
@@ -193,6 +195,8 @@ void h8_split_plan(const int32_t *Nt_order, int64_t k, int d, int sms, int64_t *
                    int *grid_small);
 size_t h8_ws_doubles(int max_N, int d);
 int h8_max_ctas_per_sm(size_t smem, int d);
+bool h8_use_small(int max_N);
+int h8_small_ctas_per_sm(size_t smem, int d);
 cudaError_t launch_h8(const Ctx &c, const double *theta_host, cudaStream_t st,
                       const double *theta_dev = nullptr);
 // One H8 launch over an explicit set of blocks (estimation or prediction mode)
@@ -212,6 +216,7 @@ struct H8Problem {
   int64_t n_big = 0;               // split launch: the first n_big work items (N > 2-CTA cap) alone
   int max_N_small = 0, grid_small = 0;
   const double *theta_d = nullptr; // graph replay: theta in device memory (H8Args::theta_d)
+  int small = 0;                   // all blocks small: the 4-warp loglik kernel (h8_use_small)
   double *Lg = nullptr;            // predict == 2: per-block factor copies
   const int64_t *lg_off = nullptr;
   const double *Xq;
