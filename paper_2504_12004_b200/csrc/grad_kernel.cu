@@ -34,10 +34,11 @@
 
 namespace sbv {
 
-#ifndef SBV_GRAD_WARPS
-#define SBV_GRAD_WARPS 4  // warps per CTA (4: two CTAs per SM at <= 255 registers)
-#endif
-constexpr int kGThreads = SBV_GRAD_WARPS * 32;
+// Warps per CTA, a template parameter: 4 (two CTAs per SM at <= 255 registers,
+// every warp owns a Z slice for b <= 128) for many blocks per CTA, 8 (one CTA
+// per SM) when the launch has few blocks per CTA and the 4-warp CTAs' long
+// blocks (b > 128: several slices per warp) set the tail (grad_shape, measured:
+// cfg2 n = 1M 27.8 vs 34.4 ms, n = 200k 8.5 vs 6.9 ms).
 
 struct GradArgs {
   const double *Lg;          // per-block (N+1) x N row-major factor copies
@@ -63,7 +64,7 @@ struct GradArgs {
 #ifndef SBV_GRAD_PF
 #define SBV_GRAD_PF 2  // k-steps of register prefetch in the DMMA loops
 #endif
-constexpr int kGSW = SBV_GRAD_SW, kGPF = SBV_GRAD_PF, kGW = kGThreads / 32;
+constexpr int kGSW = SBV_GRAD_SW, kGPF = SBV_GRAD_PF;
 
 // f(r) and h(r) = f'(r)/r of the half-integer closed forms (sigma2 = 1),
 // NU2 = 2 nu, e = e^{-r}, ri = 1/r (used by nu = 1/2 only)
@@ -117,8 +118,9 @@ __device__ __forceinline__ void gemm_pf(double (&acc)[4][NCT][2], int kb, int ke
 
 // DM > 0: coordinates staged with the padded row stride DM (d <= DM, zero
 // padded; the padded dimensions contribute 0 to every distance and gradient)
-template <int NU2, int DM>
-__global__ void __launch_bounds__(kGThreads, 8 / SBV_GRAD_WARPS) k_grad(GradArgs a) {
+template <int NU2, int DM, int NWG>
+__global__ void __launch_bounds__(32 * NWG, 8 / NWG) k_grad(GradArgs a) {
+  constexpr int kGThreads = 32 * NWG, kGW = NWG;
   extern __shared__ double gsm[];
   __shared__ int s_item;
   __shared__ double s_etab[256];
@@ -386,10 +388,20 @@ __global__ void k_grad_sum(const double *grads, int64_t k_local, int P, double *
   if (lane == 0) out[k] = s;
 }
 
-size_t grad_smem_bytes(int max_N, int d) {
+size_t grad_smem_bytes(int max_N, int d, int nw) {
   const int ds = d <= 16 ? (d <= 4 ? 4 : d <= 8 ? 8 : d <= 10 ? 10 : d <= 12 ? 12 : 16) : d;
-  return sizeof(double) * ((size_t)max_N * ds + 4 * (size_t)max_N + kGW * (size_t)(d + 2) + SBV_MAX_D +
-                           kGW * 32 * 33);
+  return sizeof(double) * ((size_t)max_N * ds + 4 * (size_t)max_N + nw * (size_t)(d + 2) + SBV_MAX_D +
+                           (size_t)nw * 32 * 33);
+}
+
+// 4 or 8 warps per CTA for a launch of k blocks on `sms` SMs (see k_grad)
+// (SBV_GRAD_NW = 4 or 8 forces one: tests cover both instantiations)
+int grad_shape(int64_t k, int sms) {
+  if (const char *e = getenv("SBV_GRAD_NW")) {
+    const int v = atoi(e);
+    if (v == 4 || v == 8) return v;
+  }
+  return k < (int64_t)16 * 2 * sms ? 8 : 4;
 }
 
 static int grad_dm(int d) {
@@ -401,30 +413,36 @@ static int grad_dm(int d) {
   return 0;
 }
 
-template <int NU2>
+template <int NU2, int NWG>
 static void (*pick_grad(int dm))(GradArgs) {
   switch (dm) {
-    case 4: return k_grad<NU2, 4>;
-    case 8: return k_grad<NU2, 8>;
-    case 10: return k_grad<NU2, 10>;
-    case 12: return k_grad<NU2, 12>;
-    case 16: return k_grad<NU2, 16>;
-    default: return k_grad<NU2, 0>;
+    case 4: return k_grad<NU2, 4, NWG>;
+    case 8: return k_grad<NU2, 8, NWG>;
+    case 10: return k_grad<NU2, 10, NWG>;
+    case 12: return k_grad<NU2, 12, NWG>;
+    case 16: return k_grad<NU2, 16, NWG>;
+    default: return k_grad<NU2, 0, NWG>;
   }
 }
 
-static void (*pick_grad_fn(double nu, int d))(GradArgs) {
+template <int NWG>
+static void (*pick_grad_nw(double nu, int dm))(GradArgs) {
+  return nu == 0.5 ? pick_grad<1, NWG>(dm) : nu == 1.5 ? pick_grad<3, NWG>(dm)
+                   : nu == 2.5 ? pick_grad<5, NWG>(dm) : pick_grad<7, NWG>(dm);
+}
+
+static void (*pick_grad_fn(double nu, int d, int nw))(GradArgs) {
   const int dm = grad_dm(d);
-  return nu == 0.5 ? pick_grad<1>(dm) : nu == 1.5 ? pick_grad<3>(dm) : nu == 2.5 ? pick_grad<5>(dm) : pick_grad<7>(dm);
+  return nw == 8 ? pick_grad_nw<8>(nu, dm) : pick_grad_nw<4>(nu, dm);
 }
 
 // persistent grid: resident CTAs per SM (shared memory / registers) x SMs
-int grad_grid(double nu, int d, int max_N, int sms) {
-  void (*f)(GradArgs) = pick_grad_fn(nu, d);
-  const size_t sm = grad_smem_bytes(max_N, d);
+int grad_grid(double nu, int d, int max_N, int sms, int nw) {
+  void (*f)(GradArgs) = pick_grad_fn(nu, d, nw);
+  const size_t sm = grad_smem_bytes(max_N, d, nw);
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kGThreads, sm) != cudaSuccess || nb < 1) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, 32 * nw, sm) != cudaSuccess || nb < 1) {
     cudaGetLastError();
     nb = 1;
   }
@@ -456,10 +474,10 @@ cudaError_t launch_grad(const GradLaunch &gl, cudaStream_t st) {
   if (e) return e;
   if (gl.n_items == 0) return cudaSuccess;
   const double nu = gl.theta[gl.d + 1];
-  void (*f)(GradArgs) = pick_grad_fn(nu, gl.d);
-  const size_t sm = grad_smem_bytes(gl.max_N, gl.d);
+  void (*f)(GradArgs) = pick_grad_fn(nu, gl.d, gl.nw);
+  const size_t sm = grad_smem_bytes(gl.max_N, gl.d, gl.nw);
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  f<<<gl.grid, kGThreads, sm, st>>>(a);
+  f<<<gl.grid, 32 * gl.nw, sm, st>>>(a);
   return cudaGetLastError();
 }
 

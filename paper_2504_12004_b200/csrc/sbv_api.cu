@@ -1007,7 +1007,8 @@ int sbv_loglik_grad(sbv_handle h, const double *y, const double *theta, double *
   const int bpad_max = ((((h->max_bs + 3) & ~3) + 1) + 31) & ~31;
   int sms = 0;
   CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-  const int ggrid = (int)std::min<int64_t>(grad_grid(theta[d + 1], d, std::max(h->max_N, 1), sms),
+  const int gnw = grad_shape(h->k_local, sms);
+  const int ggrid = (int)std::min<int64_t>(grad_grid(theta[d + 1], d, std::max(h->max_N, 1), sms, gnw),
                                            std::max<int64_t>(h->k_local, 1));
   CU(ensure(h->zws, (int64_t)ggrid * std::max(h->max_N, 1) * std::max(bpad_max, 32), cap));
   CU(ensure(h->grads, std::max<int64_t>(h->k_local, 1) * P, cap));
@@ -1059,6 +1060,7 @@ int sbv_loglik_grad(sbv_handle h, const double *y, const double *theta, double *
     gl.max_N = std::max(h->max_N, 1);
     gl.bpad_max = std::max(bpad_max, 32);
     gl.grid = (int)std::min<int64_t>(ggrid, i1 - i0);
+    gl.nw = gnw;
     gl.theta = theta;
     gl.zws = h->zws;
     gl.queue = h->queue;

@@ -233,13 +233,15 @@ struct GradLaunch {
   const int32_t *nbr, *cnt, *local_blocks, *items;
   int64_t n_items;
   int m, d, max_N, bpad_max, grid;
+  int nw;  // warps per CTA of k_grad (grad_shape)
   const double *theta;  // host
   double *zws;
   unsigned int *queue;
   double *grads;
 };
-size_t grad_smem_bytes(int max_N, int d);
-int grad_grid(double nu, int d, int max_N, int sms);
+size_t grad_smem_bytes(int max_N, int d, int nw);
+int grad_shape(int64_t k, int sms);
+int grad_grid(double nu, int d, int max_N, int sms, int nw);
 cudaError_t launch_grad(const GradLaunch &gl, cudaStream_t st);
 cudaError_t launch_grad_sum(const double *grads, int64_t k_local, int P, double *out, cudaStream_t st);
 cudaError_t launch_reduce_chunks(const Ctx &c, cudaStream_t st);

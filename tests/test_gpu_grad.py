@@ -49,6 +49,20 @@ def _check(sbv, orc, X, y, bs, m, scale, theta, name):
     return h, g
 
 
+@pytest.mark.parametrize("nw", ["4", "8"])
+def test_grad_both_cta_shapes(sbv, orc, nw, monkeypatch):
+    """k_grad's 4-warp (2 CTAs/SM) and 8-warp instantiations (grad_shape picks
+    by blocks per CTA; SBV_GRAD_NW forces one) against the oracle, N up to
+    ~420 (b > 128: several Z slices per warp)."""
+    monkeypatch.setenv("SBV_GRAD_NW", nw)
+    n, d, bs, m = 4000, 5, 150, 200
+    X = si.make_X(n, d, seed=9)
+    y = si.make_y(X, seed=10)
+    scale = si.default_scale(d)
+    theta = si.default_theta(d, nu=2.5, tau2=1e-3)
+    _check(sbv, orc, X, y, bs, m, scale, theta, f"grad_nw{nw}")
+
+
 @pytest.mark.parametrize("d,bs,m,nu", [
     (5, 20, 40, 2.5),
     (3, 10, 30, 3.5),
