@@ -267,7 +267,10 @@ struct Timer {
   int prep;
   int idx = 0;
   Timer(sbv_ctx *h_, int prep_) : h(h_), prep(prep_) {
-    if (h->profile) cudaEventRecord(h->ev[0], h->stream);
+    if (!h->profile) return;
+    h->ev_pending[prep ? 0 : 1] = 0;  // the previous call's events are being re-recorded
+    (prep ? h->n_ev_prep : h->n_ev_llh) = 0;
+    cudaEventRecord(h->ev[prep ? 0 : 1][0], h->stream);
   }
   void mark(const char *name) {
     if (h->debug) {  // SBV_DEBUG=1: stage trace on stderr (host-side progress)
@@ -275,21 +278,29 @@ struct Timer {
       fflush(stderr);
     }
     if (!h->profile || idx >= kMaxStages) return;
-    cudaEventRecord(h->ev[idx + 1], h->stream);
+    cudaEventRecord(h->ev[prep ? 0 : 1][idx + 1], h->stream);
     (prep ? h->name_prep : h->name_llh)[idx] = name;
     idx++;
   }
-  void finish() {
+  void finish() {  // no synchronisation here: sbv_stage_times resolves the events
     if (!h->profile) return;
-    cudaEventSynchronize(h->ev[idx]);
-    for (int i = 0; i < idx; i++) {
-      float ms = 0;
-      cudaEventElapsedTime(&ms, h->ev[i], h->ev[i + 1]);
-      (prep ? h->t_prep : h->t_llh)[i] = ms;
-    }
     (prep ? h->n_ev_prep : h->n_ev_llh) = idx;
+    h->ev_pending[prep ? 0 : 1] = 1;
   }
 };
+
+void resolve_stage_times(sbv_ctx *h, int prep) {
+  const int w = prep ? 0 : 1;
+  if (!h->ev_pending[w]) return;
+  const int n = prep ? h->n_ev_prep : h->n_ev_llh;
+  cudaEventSynchronize(h->ev[w][n]);
+  for (int i = 0; i < n; i++) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, h->ev[w][i], h->ev[w][i + 1]);
+    (prep ? h->t_prep : h->t_llh)[i] = ms;
+  }
+  h->ev_pending[w] = 0;
+}
 
 int validate_theta(sbv_ctx *h, const double *theta) {
   if (!theta) return fail(h, SBV_ERR_ARG, "theta is NULL");
@@ -475,7 +486,8 @@ int sbv_create(const sbv_opts *opts, sbv_handle *out) {
     h->stream = (cudaStream_t)opts->stream;
     h->profile = opts->profile;
   }
-  for (int i = 0; i <= kMaxStages; i++) cudaEventCreate(&h->ev[i]);
+  for (int w = 0; w < 2; w++)
+    for (int i = 0; i <= kMaxStages; i++) cudaEventCreate(&h->ev[w][i]);
   cudaEventCreateWithFlags(&h->ev_sizes, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&h->ev_pin, cudaEventDisableTiming);
   if (cudaMallocHost(&h->result_host, 8 * sizeof(double)) != cudaSuccess ||
@@ -501,7 +513,8 @@ void sbv_destroy(sbv_handle h) {
   free_state(h);
   if (h->comm) ncclCommDestroy(h->comm);
   for (int i = 0; i <= kMaxStages; i++)
-    if (h->ev[i]) cudaEventDestroy(h->ev[i]);
+    for (int w = 0; w < 2; w++)
+      if (h->ev[w][i]) cudaEventDestroy(h->ev[w][i]);
   if (h->ev_sizes) cudaEventDestroy(h->ev_sizes);
   if (h->ev_pin) cudaEventDestroy(h->ev_pin);
   if (h->result_host) cudaFreeHost(h->result_host);
@@ -1196,6 +1209,8 @@ int sbv_stats(sbv_handle h, double *out9) {
 int sbv_stage_times(sbv_handle h, int32_t prep, double *ms, const char **names, int32_t cap,
                     int32_t *count) {
   if (!h || !count) return SBV_ERR_ARG;
+  cudaSetDevice(h->device);
+  resolve_stage_times(h, prep);
   int nn = prep ? h->n_ev_prep : h->n_ev_llh;
   nn = std::min(nn, (int)cap);
   for (int i = 0; i < nn; i++) {

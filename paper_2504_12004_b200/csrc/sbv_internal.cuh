@@ -141,7 +141,10 @@ struct Ctx {
   int32_t err_stage = 0;
   std::string err_msg;
   // profiling
-  cudaEvent_t ev[kMaxStages + 1] = {};
+  // per-stage events of the last prepare [0] / loglik [1]; resolved lazily by
+  // sbv_stage_times, so profiling adds no host synchronisation to the calls
+  cudaEvent_t ev[2][kMaxStages + 1] = {};
+  int ev_pending[2] = {0, 0};
   int n_ev_prep = 0, n_ev_llh = 0;
   double t_prep[kMaxStages] = {}, t_llh[kMaxStages] = {};
   const char *name_prep[kMaxStages] = {}, *name_llh[kMaxStages] = {};
