@@ -44,11 +44,16 @@ for name, fn in (("h8", "h8_full_ncu_summary.json"), ("knn", "knn_full_ncu_summa
 p = os.path.join(src, f"{tag}_launches.csv")
 if os.path.exists(p):
     lines = [l for l in open(p) if l.startswith('"')]
-    rows = list(csv.DictReader(io.StringIO("".join(lines))))
+    rows = [r for r in csv.DictReader(io.StringIO("".join(lines))) if r["Metric Name"] == "gpu__time_duration.sum"]
+    # the bench steps only (3 warm-up + 3 timed = prepare from k_scale through
+    # loglik's k_final, 6 times), not the loglik-only / graph / gradient /
+    # prediction measurements that follow them in the same process
+    names = [r["Kernel Name"] for r in rows]
+    finals = [i for i, nm in enumerate(names) if "k_final" in nm]
+    if len(finals) >= 6:
+        rows = rows[: finals[5] + 1]
     tot, cnt = defaultdict(float), defaultdict(int)
     for r in rows:
-        if r["Metric Name"] != "gpu__time_duration.sum":
-            continue
         v = float(r["Metric Value"].replace(",", ""))
         scale = {"ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "nsecond": 1e-6}.get(r["Metric Unit"], 1.0)
         k = r["Kernel Name"].split("(")[0]
@@ -57,7 +62,8 @@ if os.path.exists(p):
     s = sum(tot.values())
     ks = sorted(tot, key=lambda k: -tot[k])
     json.dump({"command": "python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-predict",
-               "note": "ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised); compare SHARES, not absolute times",
+               "note": "ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised); "
+                       "the 6 bench steps (3 warm-up + 3 timed, prepare + loglik) only; compare SHARES, not absolute times",
                "tag": tag, "total_launches": sum(cnt.values()),
                "kernels": [{"kernel": k, "launches": cnt[k], "total_ms": tot[k], "share": tot[k] / s} for k in ks]},
               open(os.path.join(out, "launch_list_summary.json"), "w"), indent=1)
