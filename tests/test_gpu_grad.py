@@ -145,3 +145,26 @@ def test_grad_cfg2_full_size_central_differences(sbv):
         f.write(json.dumps({"test": "grad_cfg2_central_differences", "max_rel": float(rel.max()),
                             "rel": rel.tolist(), "rel_to_abs_g": (np.abs(g - fd) / np.abs(g)).tolist()}) + "\n")
     assert rel.max() <= TOL_G, (rel, g, fd)
+
+
+def test_block_grads_state_rules(sbv):
+    """sbv_block_grads: SBV_ERR_STATE before any sbv_loglik_grad and after a
+    re-prepare; after a gradient call its rows sum to the gradient."""
+    import torch
+    n, d, bs, m = 3000, 4, 30, 40
+    X = torch.from_numpy(si.make_X(n, d, seed=21)).cuda()
+    y = torch.from_numpy(si.make_y(si.make_X(n, d, seed=21), seed=22)).cuda()
+    theta = si.default_theta(d, nu=1.5, tau2=1e-3)
+    h = sbv.Handle(seed=3)
+    h.prepare(X, bs, m, si.default_scale(d))
+    with pytest.raises(sbv.SBVError) as e:
+        h.block_grads()
+    state = e.value.code
+    assert state == 7  # SBV_ERR_STATE
+    ll, g = h.loglik_grad(y, theta)
+    gb = h.block_grads()
+    assert np.all(np.abs(gb.sum(0) - g) <= 1e-12 * np.abs(gb).sum(0))
+    h.prepare(X, bs, m, si.default_scale(d))
+    with pytest.raises(sbv.SBVError) as e:
+        h.block_grads()
+    assert e.value.code == state
